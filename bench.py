@@ -1,0 +1,446 @@
+"""Benchmark of the sparse-TTV hot path on B200 (one JSON line on rank 0).
+
+Headline workload: BASELINE config 5 -- skewed 3-way COO tensor 1e6 x 1e5 x 1e4 with
+4e8 distinct Zipf(1.2) coordinates, N(0,1) values, contracted in mode 2 (0-based) with a
+uniform length-1e4 vector; sparse 1e6 x 1e5 result.  A "step" is one full TTV over the
+tensor (all ranks' shards), through the C ABI (tk_ttv_f64_device), including the host
+read-back of the result count.  Inputs (12.8 GB) exceed the 126 MB L2, so no flush is
+needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 5] [--nnz NNZ] [--no-secondary] [--no-e2e]
+
+N > 1: launched by torchrun, one process per GPU, NCCL; nnz sharded at key changes
+(multi.shard_bounds), the merge is an all-gather of per-rank counts inside the timed
+region; time = max over ranks of device time (CUDA events).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CFG5 = {"shape": (10**6, 10**5, 10**4), "nnz": 4 * 10**8, "k": 2, "zipf_s": 1.2, "seed": 12345, "xseed": 777}
+CFG4 = {"shape": (20000,) * 4, "nnz": 10**8, "keep": 0, "seed": 4444}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_info():
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = os.cpu_count()
+    return os.cpu_count(), aff
+
+
+# ---- CPU legs (oracle = checker / baseline only) ----------------------------------------------
+
+def cpu_reference_ttv(subs, vals, shape, x, k, repeats=1):
+    """Time the reference's own compiled kernel (oracle/_ref) or, if absent, the C port."""
+    from oracle import oracle
+    ck = oracle.reference_module()
+    best = None
+    for _ in range(repeats):
+        if ck is not None:
+            (_, v, _), el = ck.ttv_timed(subs, vals, tuple(shape), x, k)
+            kind = "reference"
+        else:
+            t0 = time.perf_counter()
+            _, v, _ = oracle.ttv_raw(subs, vals, shape, x, k)
+            el = time.perf_counter() - t0
+            kind = "port"
+        best = el if best is None else min(best, el)
+    return best, kind, len(v)
+
+
+def sample_prefix(t, rows: int):
+    """Host copy of a prefix of the device tensor, cut at a kept-key change."""
+    import torch
+    from paper_2510_01495_b200 import multi
+    rows = min(rows, t.nnz)
+    key = multi.kept_prefix_key(t.cols, t.ndim - 1, t.shape)
+    if rows < t.nnz:
+        rows = int(torch.searchsorted(key, key[rows - 1:rows], right=True).item())
+    subs = torch.stack([c[:rows] for c in t.cols], dim=1).cpu().numpy()
+    vals = t.vals[:rows].cpu().numpy()
+    return np.ascontiguousarray(subs), vals
+
+
+# ---- reference arm ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    torch.cuda.set_device(0)
+    cfg = dict(CFG5)
+    nnz = args.nnz or cfg["nnz"]
+    t = DeviceCoo.generate(cfg["shape"], nnz, zipf_s=cfg["zipf_s"], normal_vals=True, seed=cfg["seed"])
+    x = uniform_vector(cfg["shape"][2], cfg["xseed"]).cpu().numpy()
+    subs, vals = sample_prefix(t, args.cpu_sample)
+    del t
+    torch.cuda.empty_cache()
+    times = []
+    kind = "port"
+    for i in range(args.warmup + args.steps):
+        el, kind, _ = cpu_reference_ttv(subs, vals, cfg["shape"], x, cfg["k"])
+        if i >= args.warmup:
+            times.append(el)
+    ms = 1e3 * float(np.mean(times))
+    value = subs.shape[0] / (ms / 1e3)
+    ncpu, aff = cpu_info()
+    line = {
+        "impl": "reference", "metric": "sparse TTV throughput (config 5, skewed Zipf 4e8 nnz)",
+        "value": value, "unit": "nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, seeded)",
+        "config": {"workload": "cfg5_ttv_zipf_1e6x1e5x1e4_nnz4e8_mode2", "sample_rows": int(subs.shape[0]),
+                   "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": kind,
+                         "sample": f"canonical prefix of the config-5 tensor, {subs.shape[0]} rows, cut at a key change",
+                         "host_cpus": ncpu, "affinity": aff},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ---------------------------------------------------------------------------------
+
+def secondary_measurements(rank, steps):
+    """Configs 1-4 on one GPU (kernel time by CUDA events, L2 flushed between iterations)."""
+    import torch
+    from paper_2510_01495_b200 import _lib, synth
+    from paper_2510_01495_b200 import device as dv
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    lib = _lib.load()
+    flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")  # 256 MB > 126 MB L2
+    res = {}
+
+    def kernel_ms(fn):
+        ts = []
+        for i in range(steps + 2):
+            flush.zero_()
+            torch.cuda.synchronize()
+            fn()
+            if i >= 2:
+                ts.append(lib.tk_last_kernel_ms())
+        return float(np.median(ts))
+
+    ops = synth.host_operands(1)
+    x, y = torch.from_numpy(ops["x"]).cuda(), torch.from_numpy(ops["y"]).cuda()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    ms = kernel_ms(lambda: dv.dot(x, y, out))
+    res["cfg1_dot"] = {"kernel_ms": ms, "GBps": 16e6 / ms / 1e6, "bytes": 16_000_000}
+    ops = synth.host_operands(2)
+    a, xv = torch.from_numpy(ops["a"]).cuda(), torch.from_numpy(ops["x"]).cuda()
+    yv = torch.empty(4096, dtype=torch.float64, device="cuda")
+    ms = kernel_ms(lambda: dv.matvec(a, xv, yv))
+    b = 8 * (4096 * 4096 + 4096 + 4096)
+    res["cfg2_matvec"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "bytes": b}
+    ops = synth.host_operands(3)
+    t3 = ops["tensor"]
+    dt = DeviceCoo.from_host(t3.subs, t3.vals, t3.shape)
+    x3 = torch.from_numpy(ops["x"]).cuda()
+    o_s = torch.empty((t3.nnz, 2), dtype=torch.int64, device="cuda")
+    o_v = torch.empty(t3.nnz, dtype=torch.float64, device="cuda")
+    u = [0]
+
+    def run3():
+        u[0] = dt.ttv(x3, 2, o_s, o_v)[0]
+    ms = kernel_ms(run3)
+    b = t3.nnz * 32 + 8 * 1000 + u[0] * 24
+    res["cfg3_ttv"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": t3.nnz / ms * 1e3, "bytes": b, "u": u[0]}
+    del dt, o_s, o_v
+    c4 = CFG4
+    t4 = DeviceCoo.generate(c4["shape"], c4["nnz"], seed=c4["seed"])
+    vecs = {m: uniform_vector(c4["shape"][m], 40 + m) for m in (1, 2, 3)}
+    out4 = torch.empty(c4["shape"][0], dtype=torch.float64, device="cuda")
+    ms = kernel_ms(lambda: t4.ttv_dense(vecs, 0, out4))
+    b = c4["nnz"] * 40 + 3 * 8 * 20000 + 8 * 20000
+    res["cfg4_ttv_dense"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c4["nnz"] / ms * 1e3, "bytes": b}
+    del t4
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args):
+    import torch
+    from paper_2510_01495_b200 import _lib, multi
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    rank, world, local = dist_setup(args)
+    lib = _lib.load()
+    cfg = dict(CFG5)
+    nnz_total = args.nnz or cfg["nnz"]
+    shape, k = cfg["shape"], cfg["k"]
+
+    # ---- operands (outside the timed region) ----
+    t_gen = time.perf_counter()
+    full = DeviceCoo.generate(shape, nnz_total, zipf_s=cfg["zipf_s"], normal_vals=True, seed=cfg["seed"])
+    gen_s = time.perf_counter() - t_gen
+    x = uniform_vector(shape[k], cfg["xseed"])
+    key = multi.kept_prefix_key(full.cols, 2, shape)
+    bounds = multi.shard_bounds(key, world)
+    del key
+    lo, hi = bounds[rank], bounds[rank + 1]
+    t = full.slice(lo, hi, copy=True) if world > 1 else full
+    cpu_leg = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        subs_s, vals_s = sample_prefix(full, args.cpu_sample)
+    if world > 1:
+        del full
+    torch.cuda.empty_cache()
+    n_local = t.nnz
+    out_subs = torch.empty((max(n_local, 1), 2), dtype=torch.int64, device="cuda")
+    out_vals = torch.empty(max(n_local, 1), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        u, _, _ = t.ttv(x, k, out_subs, out_vals)
+        if world > 1:
+            counts = multi.gather_counts(u, torch.device("cuda"))
+            return u, counts
+        return u, [u]
+
+    for _ in range(args.warmup):
+        u_local, counts = step()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----
+    kms = []
+    launches0 = lib.tk_launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            u_local, counts = step()
+            kms.append(lib.tk_last_kernel_ms())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = lib.tk_launch_count() - launches0
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    u_total = sum(counts)
+    value = nnz_total / (ms / 1e3)
+
+    # roofline of the dominant kernel (the streaming TTV), per launch, this rank's shard
+    kern_ms = float(np.mean(kms))
+    alg_bytes = n_local * 32 + 8 * shape[k] + u_local * 24
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        if tj.get("nnz") == n_local:
+            traffic = tj.get("dram_bytes_per_launch")
+
+    # ---- e2e through the host-buffer C ABI (pinned host in, host out) ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(t, x, k, args, world)
+
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        del out_subs, out_vals
+        torch.cuda.empty_cache()
+        secondary = secondary_measurements(rank, max(3, min(args.steps, 10)))
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        el, kind, _ = cpu_reference_ttv(subs_s, vals_s, shape, x.cpu().numpy(), k)
+        cpu_leg = {"value": subs_s.shape[0] / el, "unit": "nnz/s", "cores": 1, "kind": kind,
+                   "sample": f"canonical prefix of the config-5 tensor, {subs_s.shape[0]} rows "
+                             f"(cut at a key change), one call",
+                   "host_cpus": cpu_info()[0], "affinity": cpu_info()[1], "seconds": el}
+
+    if rank == 0:
+        line = {
+            "metric": "sparse TTV throughput (config 5, skewed Zipf 4e8 nnz)",
+            "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (device-generated, seeded; Zipf(1.2) coords, N(0,1) vals)",
+            "config": {"workload": "cfg5_ttv_zipf_1e6x1e5x1e4_nnz4e8_mode2", "nnz": nnz_total, "shape": shape,
+                       "mode": k, "u": u_total, "parallelism": f"nnz-shard{world}",
+                       "l2": "inputs (12.8 GB) larger than L2; no flush", "gen_seconds": round(gen_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "seg_ttv_kernel<Raw,2,8>", "kernel_ms": kern_ms,
+                         "alg_bytes_per_launch": alg_bytes},
+            "clocks": clocks.summary(),
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu_leg,
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(t, x, k, args, world):
+    """Host-buffer path: tk_ttv_f64_host with pinned inputs/outputs, copies timed."""
+    import ctypes
+    import torch
+    from paper_2510_01495_b200 import _lib
+    lib = _lib.load()
+    n = t.nnz
+    subs_h = torch.empty((n, 3), dtype=torch.int64, pin_memory=True)
+    subs_h.copy_(torch.stack(t.cols, dim=1))
+    vals_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    vals_h.copy_(t.vals.cpu())
+    x_h = x.cpu().pin_memory()
+    os_h = torch.empty((n, 2), dtype=torch.int64, pin_memory=True)
+    ov_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    u = ctypes.c_int64(0)
+    shp = _lib.i64_array(t.shape)
+
+    def call():
+        _lib.check(lib.tk_ttv_f64_host(3, shp, n, subs_h.data_ptr(), vals_h.data_ptr(), x_h.data_ptr(),
+                                       int(x_h.shape[0]), k, os_h.data_ptr(), ov_h.data_ptr(), ctypes.byref(u)))
+
+    call()
+    steps = max(1, min(args.e2e_steps, args.steps))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    el = (time.perf_counter() - t0) / steps
+    el = max_over_ranks(el, world)
+    total = n * world if world == 1 else None
+    nnz_total = args.nnz or CFG5["nnz"]
+    return {"value": nnz_total / el, "unit": "nnz/s", "h2d_bytes_per_step": int(n * 32 + 8 * x_h.shape[0]),
+            "d2h_bytes_per_step": int(u.value * 24), "ms_per_step": el * 1e3, "steps": steps,
+            "path": "tk_ttv_f64_host (pinned host row-major subs/vals -> HBM -> kernels -> host)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nnz", type=int, default=0, help="override config-5 nnz (debug only)")
+    ap.add_argument("--cpu-sample", type=int, default=40_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

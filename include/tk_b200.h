@@ -1,0 +1,151 @@
+/*
+ * tk_b200.h -- C ABI of libtk_b200.so, the B200 (sm_100a) kernel library behind the
+ * drop-in kernel module paper_2510_01495_b200 (BACKEND "b200").
+ *
+ * It replaces the reference's native kernel module, pkg/src/tenkern/_ckernels.pyx,
+ * which the reference reaches through its kernel-module protocol
+ * (pkg/src/tenkern/backend.py:33-49) and its FFI wrapper BoundKernelSet
+ * (pkg/hostbench/src/tenhost/bindings.py:40-79).  Each entry point below names the
+ * reference function whose contract it carries.
+ *
+ * Conventions
+ *   - every function returns a tk_status; on failure tk_last_error() holds a message
+ *     (thread-local) worded like the reference's exception text;
+ *   - *_device functions take DEVICE pointers and a cudaStream_t passed as void*;
+ *     they return after the result (and *out_nnz) is final on the host;
+ *   - *_host functions take HOST pointers (pinned or pageable) and move the data
+ *     themselves: this is the call a cgo / JNI / ctypes binding of the reference's
+ *     ttv_raw / dot / matvec would make;
+ *   - inputs are borrowed read-only (the reference takes const memoryviews,
+ *     _ckernels.pyx:40, 48, 129), outputs are caller-owned;
+ *   - mode numbers are 0-based like tenkern.ttv (sparse.py:213);
+ *   - subs are int64; vals / vectors float64 (the reference's boundary dtypes,
+ *     bindings.py:19-37);
+ *   - one call at a time per device (the reference is single-threaded).
+ */
+#ifndef TK_B200_H
+#define TK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tk_status {
+  TK_OK = 0,
+  TK_EDIM = 1,     /* tenkern.DimensionError  (lengths / shapes / mode-k index)       */
+  TK_EMODE = 2,    /* tenkern.ModeError       (k outside [0, d))                       */
+  TK_EORDER = 3,   /* tenkern.OrderError      (d < 2)                                  */
+  TK_EINDEX = 4,   /* tenkern.DimensionError  (mode-k index outside x, pyx:361-365)    */
+  TK_ECUDA = 6,    /* CUDA runtime failure                                             */
+  TK_EARG = 8,     /* unsupported argument (e.g. order > TK_MAX_ORDER, null pointer)   */
+  TK_ENOMEM = 9    /* device allocation failed                                         */
+} tk_status;
+
+#define TK_MAX_ORDER 16
+
+/* Message for the last failing call on this thread ("" if none). */
+const char* tk_last_error(void);
+/* ABI version: major*10000 + minor*100 + patch. */
+int tk_version(void);
+/* Seconds spent inside the last *_host call on this thread, measured on the native side
+ * with a monotonic clock (the reference's *_timed protocol, _ckernels.pyx:98-122, 377-388). */
+double tk_last_call_seconds(void);
+/* Number of visible CUDA devices (0 when none). */
+int tk_device_count(int* n);
+
+/* ---- dense kernels ---------------------------------------------------------------------- */
+
+/* Sum_i x[i]*y[i] -> *out (device double).  Replaces _ckernels.dot / _dot_impl
+ * (_ckernels.pyx:40-45, 76-83).  Parallel tree order: within 1e-12 relative of the
+ * reference's left-to-right sum (documented deviation). */
+int tk_dot_f64_device(const double* x, const double* y, int64_t n, double* out, void* stream);
+/* Same with host operands and a host result; copies included. */
+int tk_dot_f64_host(const double* x, const double* y, int64_t n, double* out);
+
+/* y[i] = Sum_j A[i*cols+j]*x[j], A row-major.  Replaces _ckernels.matvec / _matvec_impl
+ * (_ckernels.pyx:48-56, 86-95). */
+int tk_matvec_f64_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, void* stream);
+int tk_matvec_f64_host(const double* a, int64_t rows, int64_t cols, const double* x, double* y);
+
+/* ---- sparse tensor-times-vector ---------------------------------------------------------- */
+
+/* Mode-k TTV of a COO tensor; sparse result in canonical form.
+ * Replaces _ckernels.ttv_raw / _ttv_pipeline (_ckernels.pyx:313-374).
+ *
+ *   d, shape[d]        tensor order and shape (host array)
+ *   nnz                stored entries
+ *   cols               host array of d DEVICE pointers, cols[m][r] = subs[r, m] (SoA);
+ *                      or NULL, then `subs` is a DEVICE row-major (nnz, d) array
+ *   vals[nnz], x[nx]   device
+ *   k                  contracted mode (0-based)
+ *   out_subs           device, capacity nnz*(d-1), written row-major (u, d-1)
+ *   out_vals           device, capacity nnz
+ *   out_nnz            HOST: number u of output entries
+ * Values are bit-identical to the reference: each group is summed left to right in
+ * ascending original-row order with round-to-nearest adds, exact zeros dropped. */
+int tk_ttv_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                      const int64_t* subs, const double* vals, const double* x, int64_t nx, int32_t k,
+                      int64_t* out_subs, double* out_vals, int64_t* out_nnz, void* stream);
+
+/* Host-buffer form of tk_ttv_f64_device: subs row-major (nnz, d) int64, vals, x on the host;
+ * out_subs (capacity nnz*(d-1)) and out_vals (capacity nnz) on the host.  This is the exact
+ * argument list of the reference's ttv_raw(subs, vals, shape, x, k) (_ckernels.pyx:370-374,
+ * bindings.py:68-79) flattened to pointers. */
+int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
+                    const double* x, int64_t nx, int32_t k, int64_t* out_subs, double* out_vals,
+                    int64_t* out_nnz);
+
+/* Unique rows of keys (host, row-major (n, m) int64) in lexicographic order with the sum
+ * of their weights, each group summed left to right in ascending original-row order; zero
+ * sums are KEPT.  Replaces tenkern.unique_rows_accumulate (sparse.py:179-197,
+ * _pykernels.py:43-68), which also canonicalises SparseCooTensor input (sparse.py:90-99).
+ * out_keys capacity n*m, out_sums capacity n (host). */
+int tk_group_sum_f64_host(int64_t n, int32_t m, const int64_t* keys, const double* weights, int64_t* out_keys,
+                          double* out_sums, int64_t* out_u);
+
+/* Multi-vector TTV to a dense vector: every mode except `keep` is contracted with
+ * vecs[m] (host array of d device pointers, vecs[keep] ignored), out[shape[keep]] dense.
+ * Defined as the chained single-mode ttv in descending mode order followed by densify
+ * (the reference has no multi-vector TTV).  Canonical input with
+ * keep == 0 takes the fused single-pass kernel (values within 1e-12 relative of the chain);
+ * anything else runs the chain on the GPU. */
+int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                            const int64_t* subs, const double* vals, int32_t keep, const double* const* vecs,
+                            double* out, void* stream);
+
+/* ---- synthetic operands (measurement inputs, generated on the device) ------------------- */
+
+/* Exactly nnz distinct coordinates of a d-way tensor, drawn per mode from a truncated
+ * Zipf(s) law on {0..shape[m]-1} (s <= 0: uniform), seeded counter-based RNG; the set is
+ * the first nnz distinct draws of the sequence.  Sorted canonical SoA output
+ * cols[m] (device, capacity nnz each).  vals: uniform [0,1) (normal_vals=0) or N(0,1)
+ * (normal_vals=1), exact zeros redrawn.  Mirrors the exact-nnz protocol of gen_sparse3
+ * (synth.py:103-143) generalised to order d and skewed coordinates (BASELINE configs 4, 5). */
+int tk_gen_coo_device(int32_t d, const int64_t* shape, int64_t nnz, double zipf_s, int32_t normal_vals,
+                      uint64_t seed, int64_t* const* cols, double* vals, void* stream);
+/* Uniform [0,1) vector from the same counter-based generator. */
+int tk_gen_uniform_device(int64_t n, uint64_t seed, double* out, void* stream);
+
+/* ---- timing helper ----------------------------------------------------------------------- */
+/* Device milliseconds between two points on a stream (cudaEvent pair). */
+int tk_timer_start(void* stream);
+int tk_timer_stop(void* stream, float* ms);
+
+/* Device milliseconds of the primary kernel(s) of the last call on this thread (the
+ * streaming TTV kernel, the dense TTV kernel, dot's two reduction kernels, matvec), from
+ * cudaEvents recorded on the launching stream; -1 if none.  Used for roofline reporting. */
+double tk_last_kernel_ms(void);
+/* Number of kernels this library has launched in this process (instrumentation). */
+long long tk_launch_count(void);
+
+/* Release cached device memory (pool trim) and pinned scratch. */
+int tk_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TK_B200_H */

@@ -1,0 +1,417 @@
+// tk_abi.cu -- extern "C" surface of libtk_b200.so (declared in include/tk_b200.h).
+//
+// Argument validation mirrors the reference's structural guards, which stay on even
+// for unchecked calls (_check_ttv, pkg/src/tenkern/_ckernels.pyx:298-310): order >= 2,
+// 0 <= k < d, len(x) == shape[k]; messages use the reference's wording so the Python
+// layer can raise the same exception text.
+#include <chrono>
+#include <cstdio>
+#include <climits>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tk_host.h"
+
+namespace tk {
+
+int gen_coo(int d, const int64_t* shape, int64_t nnz, double zipf_s, int normal_vals, uint64_t seed,
+            int64_t* const* cols, double* vals, cudaStream_t st);
+int gen_uniform(int64_t n, uint64_t seed, double* out, cudaStream_t st);
+
+namespace {
+thread_local std::string g_err;
+thread_local void* g_pinned = nullptr;
+thread_local size_t g_pinned_bytes = 0;
+thread_local cudaStream_t g_stream[64] = {};
+thread_local cudaEvent_t g_ev[64][2] = {};
+std::mutex g_mu;
+bool g_pool_ready[64] = {};
+int g_sms[64] = {};
+
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+
+cudaStream_t lib_stream() {
+  const int dev = cur_dev();
+  if (!g_stream[dev]) cudaStreamCreateWithFlags(&g_stream[dev], cudaStreamNonBlocking);
+  return g_stream[dev];
+}
+
+std::string fmt(const char* f, long long a, long long b = 0, long long c = 0) {
+  char buf[256];
+  snprintf(buf, sizeof buf, f, a, b, c);
+  return buf;
+}
+
+int check_ttv_args(int d, const int64_t* shape, int k, int64_t nx) {
+  if (d < 2) return fail(TK_EORDER, fmt("ttv: tensor order must be at least 2, got %lld", d));
+  if (k < 0 || k >= d) return fail(TK_EMODE, fmt("ttv: mode %lld out of range for order-%lld tensor", k, d));
+  if (d > TK_MAX_ORDER) return fail(TK_EARG, fmt("ttv: tensor order %lld exceeds TK_MAX_ORDER (%lld)", d, TK_MAX_ORDER));
+  if (shape == nullptr) return fail(TK_EARG, "ttv: shape is NULL");
+  if (nx != shape[k])
+    return fail(TK_EDIM, fmt("ttv: vector length %lld does not match shape[%lld] == %lld", nx, k, shape[k]));
+  return TK_OK;
+}
+
+int64_t pitch_of(int64_t n) { return (n + 1) & ~int64_t(1); }  // keep SoA columns 16-byte aligned
+
+// Native-side monotonic clock around each *_host call, like the reference's _monotonic()
+// around its kernels (_ckernels.pyx:30-33, 98-122, 377-388): excludes the FFI crossing.
+thread_local double g_last_call_s = 0.0;
+thread_local cudaEvent_t g_kev[64][2] = {};
+thread_local bool g_kev_used[64] = {};
+std::atomic<long long> g_launches{0};
+struct CallClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~CallClock() {
+    g_last_call_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int status, const std::string& msg) {
+  set_error(msg);
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")");
+  cudaGetLastError();
+  return e == cudaErrorMemoryAllocation ? TK_ENOMEM : TK_ECUDA;
+}
+
+void prepare_pool() {
+  const int dev = cur_dev();
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_pool_ready[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  g_pool_ready[dev] = true;
+}
+
+int DevBuf::alloc(size_t bytes, cudaStream_t st) {
+  reset();
+  prepare_pool();
+  if (bytes == 0) bytes = 256;
+  cudaError_t e = cudaMallocAsync(&ptr_, bytes, st);
+  if (e != cudaSuccess) {
+    ptr_ = nullptr;
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  bytes_ = bytes;
+  st_ = st;
+  return TK_OK;
+}
+
+void DevBuf::reset() {
+  if (ptr_) cudaFreeAsync(ptr_, st_);
+  ptr_ = nullptr;
+  bytes_ = 0;
+}
+
+void* pinned_scratch(size_t bytes) {
+  if (bytes > g_pinned_bytes) {
+    if (g_pinned) cudaFreeHost(g_pinned);
+    g_pinned = nullptr;
+    g_pinned_bytes = 0;
+    if (cudaMallocHost(&g_pinned, std::max<size_t>(bytes, 4096)) == cudaSuccess)
+      g_pinned_bytes = std::max<size_t>(bytes, 4096);
+  }
+  return g_pinned;
+}
+
+void ktimer_begin(cudaStream_t st) {
+  const int dev = cur_dev();
+  for (int i = 0; i < 2; ++i)
+    if (!g_kev[dev][i]) cudaEventCreate(&g_kev[dev][i]);
+  cudaEventRecord(g_kev[dev][0], st);
+  g_kev_used[dev] = false;
+}
+
+void ktimer_end(cudaStream_t st) {
+  const int dev = cur_dev();
+  cudaEventRecord(g_kev[dev][1], st);
+  g_kev_used[dev] = true;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int num_sms() {
+  const int dev = cur_dev();
+  if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return g_sms[dev] ? g_sms[dev] : 148;
+}
+
+}  // namespace tk
+
+using namespace tk;
+
+extern "C" {
+
+const char* tk_last_error(void) { return g_err.c_str(); }
+
+int tk_version(void) { return 100; }
+
+double tk_last_call_seconds(void) { return g_last_call_s; }
+
+double tk_last_kernel_ms(void) {
+  const int dev = cur_dev();
+  if (!g_kev_used[dev]) return -1.0;
+  float ms = -1.f;
+  if (cudaEventSynchronize(g_kev[dev][1]) != cudaSuccess) return -1.0;
+  if (cudaEventElapsedTime(&ms, g_kev[dev][0], g_kev[dev][1]) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+long long tk_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int tk_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *n = c;
+  return TK_OK;
+}
+
+// ---- dense ------------------------------------------------------------------------------------
+
+int tk_dot_f64_device(const double* x, const double* y, int64_t n, double* out, void* stream) {
+  if (n < 0) return fail(TK_EARG, "dot: negative length");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = dot_device(x, y, n, out, st)) return rc;
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
+int tk_dot_f64_host(const double* x, const double* y, int64_t n, double* out) {
+  CallClock clock_;
+  if (n < 0) return fail(TK_EARG, "dot: negative length");
+  cudaStream_t st = lib_stream();
+  const int64_t pn = pitch_of(n);
+  DevBuf b;
+  if (int rc = b.alloc((size_t)(2 * pn + 2) * 8, st)) return rc;
+  double* dx = b.as<double>();
+  double* dy = dx + pn;
+  double* dout = dy + pn;
+  if (n) {
+    TK_CUDA(cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, st));
+    TK_CUDA(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (int rc = dot_device(dx, dy, n, dout, st)) return rc;
+  double* h = static_cast<double*>(pinned_scratch(8));
+  TK_CUDA(cudaMemcpyAsync(h, dout, 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  *out = *h;
+  return TK_OK;
+}
+
+int tk_matvec_f64_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, void* stream) {
+  if (rows < 0 || cols < 0) return fail(TK_EARG, "matvec: negative shape");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = matvec_device(a, rows, cols, x, y, st)) return rc;
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
+int tk_matvec_f64_host(const double* a, int64_t rows, int64_t cols, const double* x, double* y) {
+  CallClock clock_;
+  if (rows < 0 || cols < 0) return fail(TK_EARG, "matvec: negative shape");
+  if (rows == 0) return TK_OK;
+  cudaStream_t st = lib_stream();
+  const size_t na = (size_t)rows * cols, pa = (na + 1) & ~size_t(1), px = ((size_t)cols + 1) & ~size_t(1);
+  DevBuf b;
+  if (int rc = b.alloc((pa + px + rows + 2) * 8, st)) return rc;
+  double* da = b.as<double>();
+  double* dx = da + pa;
+  double* dy = dx + px;
+  if (na) TK_CUDA(cudaMemcpyAsync(da, a, na * 8, cudaMemcpyHostToDevice, st));
+  if (cols) TK_CUDA(cudaMemcpyAsync(dx, x, (size_t)cols * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = matvec_device(da, rows, cols, dx, dy, st)) return rc;
+  TK_CUDA(cudaMemcpyAsync(y, dy, (size_t)rows * 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
+// ---- sparse -----------------------------------------------------------------------------------
+
+int tk_ttv_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const int64_t* subs,
+                      const double* vals, const double* x, int64_t nx, int32_t k, int64_t* out_subs,
+                      double* out_vals, int64_t* out_nnz, void* stream) {
+  if (int rc = check_ttv_args(d, shape, k, nx)) return rc;
+  if (nnz < 0 || out_nnz == nullptr) return fail(TK_EARG, "ttv: bad nnz / out_nnz");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  *out_nnz = 0;
+  if (nnz == 0) return TK_OK;
+  DevBuf soa;
+  std::vector<const int64_t*> cp(d);
+  if (cols) {
+    for (int m = 0; m < d; ++m) cp[m] = cols[m];
+  } else {
+    if (!subs) return fail(TK_EARG, "ttv: neither cols nor subs given");
+    const int64_t pitch = pitch_of(nnz);
+    if (int rc = soa.alloc((size_t)pitch * d * 8, st)) return rc;
+    if (int rc = aos_to_soa(nnz, d, subs, soa.as<int64_t>(), pitch, st)) return rc;
+    for (int m = 0; m < d; ++m) cp[m] = soa.as<int64_t>() + (size_t)m * pitch;
+  }
+  return ttv_sparse_device(d, shape, nnz, cp.data(), vals, x, nx, k, out_subs, out_vals, out_nnz, st);
+}
+
+int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
+                    const double* x, int64_t nx, int32_t k, int64_t* out_subs, double* out_vals, int64_t* out_nnz) {
+  CallClock clock_;
+  if (int rc = check_ttv_args(d, shape, k, nx)) return rc;
+  if (nnz < 0 || out_nnz == nullptr) return fail(TK_EARG, "ttv: bad nnz / out_nnz");
+  *out_nnz = 0;
+  if (nnz == 0) return TK_OK;
+  cudaStream_t st = lib_stream();
+  const int64_t pitch = pitch_of(nnz);
+  const int nk = d - 1;
+  DevBuf b_aos, b_soa, b_vals, b_x, b_os, b_ov;
+  if (int rc = b_aos.alloc((size_t)nnz * d * 8, st)) return rc;
+  if (int rc = b_soa.alloc((size_t)pitch * d * 8, st)) return rc;
+  if (int rc = b_vals.alloc((size_t)nnz * 8, st)) return rc;
+  if (int rc = b_x.alloc((size_t)std::max<int64_t>(nx, 1) * 8, st)) return rc;
+  if (int rc = b_os.alloc((size_t)nnz * nk * 8, st)) return rc;
+  if (int rc = b_ov.alloc((size_t)nnz * 8, st)) return rc;
+  TK_CUDA(cudaMemcpyAsync(b_aos.get(), subs, (size_t)nnz * d * 8, cudaMemcpyHostToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(b_vals.get(), vals, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+  if (nx) TK_CUDA(cudaMemcpyAsync(b_x.get(), x, (size_t)nx * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = aos_to_soa(nnz, d, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
+  b_aos.reset();
+  std::vector<const int64_t*> cp(d);
+  for (int m = 0; m < d; ++m) cp[m] = b_soa.as<int64_t>() + (size_t)m * pitch;
+  int64_t u = 0;
+  if (int rc = ttv_sparse_device(d, shape, nnz, cp.data(), b_vals.as<double>(), b_x.as<double>(), nx, k,
+                                 b_os.as<int64_t>(), b_ov.as<double>(), &u, st))
+    return rc;
+  if (u) {
+    TK_CUDA(cudaMemcpyAsync(out_subs, b_os.get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaMemcpyAsync(out_vals, b_ov.get(), (size_t)u * 8, cudaMemcpyDeviceToHost, st));
+  }
+  TK_CUDA(cudaStreamSynchronize(st));
+  *out_nnz = u;
+  return TK_OK;
+}
+
+int tk_group_sum_f64_host(int64_t n, int32_t m, const int64_t* keys, const double* weights, int64_t* out_keys,
+                          double* out_sums, int64_t* out_u) {
+  CallClock clock_;
+  if (n < 0 || m < 1 || m + 1 > TK_MAX_ORDER || !out_u) return fail(TK_EARG, "group_sum: bad arguments");
+  *out_u = 0;
+  if (n == 0) return TK_OK;
+  cudaStream_t st = lib_stream();
+  const int d = m + 1;
+  const int64_t pitch = pitch_of(n);
+  DevBuf b_aos, b_soa, b_w, b_one, b_os, b_ov;
+  if (int rc = b_aos.alloc((size_t)n * m * 8, st)) return rc;
+  if (int rc = b_soa.alloc((size_t)pitch * d * 8, st)) return rc;
+  if (int rc = b_w.alloc((size_t)n * 8, st)) return rc;
+  if (int rc = b_one.alloc(16, st)) return rc;
+  if (int rc = b_os.alloc((size_t)n * m * 8, st)) return rc;
+  if (int rc = b_ov.alloc((size_t)n * 8, st)) return rc;
+  static const double one = 1.0;
+  TK_CUDA(cudaMemcpyAsync(b_aos.get(), keys, (size_t)n * m * 8, cudaMemcpyHostToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(b_w.get(), weights, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(b_one.get(), &one, 8, cudaMemcpyHostToDevice, st));
+  if (int rc = aos_to_soa(n, m, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
+  TK_CUDA(cudaMemsetAsync(b_soa.as<int64_t>() + (size_t)m * pitch, 0, (size_t)n * 8, st));
+  std::vector<const int64_t*> cp(d);
+  for (int c = 0; c < d; ++c) cp[c] = b_soa.as<int64_t>() + (size_t)c * pitch;
+  // keys are arbitrary int64: declare unbounded kept dims so the sort path compares raw values
+  std::vector<int64_t> shape(d, INT64_MAX);
+  shape[m] = 1;
+  int64_t u = 0;
+  // w = weight * 1.0 is exact, so this is the reference's group-by-sum in original row order
+  if (int rc = ttv_sparse_device(d, shape.data(), n, cp.data(), b_w.as<double>(), b_one.as<double>(), 1, m,
+                                 b_os.as<int64_t>(), b_ov.as<double>(), &u, st, /*keep_zeros=*/true))
+    return rc;
+  if (u) {
+    TK_CUDA(cudaMemcpyAsync(out_keys, b_os.get(), (size_t)u * m * 8, cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaMemcpyAsync(out_sums, b_ov.get(), (size_t)u * 8, cudaMemcpyDeviceToHost, st));
+  }
+  TK_CUDA(cudaStreamSynchronize(st));
+  *out_u = u;
+  return TK_OK;
+}
+
+int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                            const int64_t* subs, const double* vals, int32_t keep, const double* const* vecs,
+                            double* out, void* stream) {
+  if (d < 2) return fail(TK_EORDER, fmt("ttv: tensor order must be at least 2, got %lld", d));
+  if (keep < 0 || keep >= d) return fail(TK_EMODE, fmt("ttv: mode %lld out of range for order-%lld tensor", keep, d));
+  if (d > TK_MAX_ORDER) return fail(TK_EARG, "ttv: tensor order exceeds TK_MAX_ORDER");
+  if (nnz < 0 || !shape || !vecs || !out) return fail(TK_EARG, "ttv_dense: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DevBuf soa;
+  std::vector<const int64_t*> cp(d);
+  if (cols) {
+    for (int m = 0; m < d; ++m) cp[m] = cols[m];
+  } else {
+    const int64_t pitch = pitch_of(nnz);
+    if (int rc = soa.alloc((size_t)pitch * d * 8, st)) return rc;
+    if (int rc = aos_to_soa(nnz, d, subs, soa.as<int64_t>(), pitch, st)) return rc;
+    for (int m = 0; m < d; ++m) cp[m] = soa.as<int64_t>() + (size_t)m * pitch;
+  }
+  return ttv_dense_device(d, shape, nnz, cp.data(), vals, keep, vecs, out, st);
+}
+
+// ---- generators -------------------------------------------------------------------------------
+
+int tk_gen_coo_device(int32_t d, const int64_t* shape, int64_t nnz, double zipf_s, int32_t normal_vals,
+                      uint64_t seed, int64_t* const* cols, double* vals, void* stream) {
+  if (d < 1 || d > TK_MAX_ORDER || !shape || !cols || !vals || nnz < 0) return fail(TK_EARG, "gen: bad arguments");
+  for (int m = 0; m < d; ++m)
+    if (shape[m] <= 0) return fail(TK_EARG, "gen: shape entries must be positive");
+  return gen_coo(d, shape, nnz, zipf_s, normal_vals, seed, cols, vals, static_cast<cudaStream_t>(stream));
+}
+
+int tk_gen_uniform_device(int64_t n, uint64_t seed, double* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = gen_uniform(n, seed, out, st)) return rc;
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
+// ---- timing -----------------------------------------------------------------------------------
+
+int tk_timer_start(void* stream) {
+  const int dev = cur_dev();
+  for (int i = 0; i < 2; ++i)
+    if (!g_ev[dev][i]) TK_CUDA(cudaEventCreate(&g_ev[dev][i]));
+  TK_CUDA(cudaEventRecord(g_ev[dev][0], static_cast<cudaStream_t>(stream)));
+  return TK_OK;
+}
+
+int tk_timer_stop(void* stream, float* ms) {
+  const int dev = cur_dev();
+  if (!g_ev[dev][0]) return fail(TK_EARG, "timer: tk_timer_start was not called");
+  TK_CUDA(cudaEventRecord(g_ev[dev][1], static_cast<cudaStream_t>(stream)));
+  TK_CUDA(cudaEventSynchronize(g_ev[dev][1]));
+  TK_CUDA(cudaEventElapsedTime(ms, g_ev[dev][0], g_ev[dev][1]));
+  return TK_OK;
+}
+
+int tk_release(void) {
+  int dev = cur_dev();
+  cudaDeviceSynchronize();
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  if (g_pinned) cudaFreeHost(g_pinned);
+  g_pinned = nullptr;
+  g_pinned_bytes = 0;
+  return TK_OK;
+}
+
+}  // extern "C"

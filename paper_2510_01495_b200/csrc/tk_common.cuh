@@ -1,0 +1,128 @@
+// tk_common.cuh -- shared device helpers for the sm_100a kernels of tk-b200.
+//
+// Everything on the TTV/dot/matvec path is an FP64, HBM-bandwidth-bound stream
+// (<= 0.125 FLOP/B), so the helpers here are about moving bytes: 1-D TMA bulk
+// copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier, relaxed
+// GPU-scope loads/stores for the decoupled look-back, and a streaming L2
+// policy for data that is read exactly once.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tk {
+
+constexpr int kMaxOrder = 16;              // largest tensor order the GPU path accepts
+constexpr int kMaxKeep = kMaxOrder - 1;    // kept (output) modes
+
+// device-side status bits, collected in Counters::flags
+enum : unsigned int {
+  kFlagIndex = 1u,     // contracted-mode index outside x -> DimensionError
+  kFlagUnsorted = 2u,  // kept-mode keys not non-decreasing -> take the sort path
+  kFlagKeptOob = 4u,   // kept-mode index outside its dimension (garbage input)
+};
+
+// Per-call scalars written by the kernels and read back by the host once.
+struct Counters {
+  unsigned long long groups;     // number of output groups (before zero elimination)
+  unsigned long long zeros;      // groups whose serial sum is exactly 0.0
+  unsigned int flags;            // kFlag* bits
+  unsigned int tile_ticket;      // dynamic tile ids (in launch order) for look-back
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier + 1-D bulk async copy (TMA engine, no tensor map needed) ----------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// bytes must be a multiple of 16, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// ---- relaxed GPU-scope accesses for the look-back status words ------------------------------
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Streaming 8-byte loads that should not displace reusable lines.
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+  return __ldcs(p);
+}
+
+// ---- decoupled look-back over per-tile counts ----------------------------------------------
+// status word: [63:62] = 0 invalid, 1 aggregate, 2 inclusive prefix; [61:0] = count.
+constexpr unsigned long long kStAgg = 1ull << 62;
+constexpr unsigned long long kStPre = 2ull << 62;
+constexpr unsigned long long kStVal = (1ull << 62) - 1;
+
+// Called by one full warp.  Publishes `agg` for `tile` and returns the exclusive prefix
+// (sum of the aggregates of all tiles < tile).  Tiles are handed out in launch order by
+// Counters::tile_ticket, so every predecessor is resident or finished (forward progress).
+__device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long long* status, long long tile,
+                                                                 unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(status, kStPre | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed(status + tile, kStAgg | agg);
+  unsigned long long excl = 0;
+  long long look = tile - 1;
+  while (true) {
+    long long t = look - lane;
+    unsigned long long s = t >= 0 ? ld_relaxed(status + t) : kStPre;
+    while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
+      if ((s >> 62) == 0) s = ld_relaxed(status + t);
+    }
+    unsigned int pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    unsigned long long v = (pre && lane > __ffs(pre) - 1) ? 0ull : (s & kStVal);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (pre) break;
+    look -= 32;
+  }
+  if (lane == 0) st_relaxed(status + tile, kStPre | (excl + agg));
+  return excl;
+}
+
+}  // namespace tk

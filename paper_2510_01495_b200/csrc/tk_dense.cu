@@ -1,0 +1,170 @@
+// tk_dense.cu -- dot and row-major matvec for sm_100a (FP64, HBM-bound streams).
+//
+// Reference: _dot_impl / _matvec_impl, pkg/src/tenkern/_ckernels.pyx:40-56 (one scalar
+// accumulator, left to right).  A single dependency chain over 1e6 adds cannot use a GPU,
+// so both kernels reduce in a fixed tree order: grid-stride 128-bit loads, per-thread
+// partial sums, warp-shuffle butterflies, a fixed-order block and grid combine.  The
+// result is deterministic run to run and within 1e-12 relative of the reference's
+// left-to-right sum (north-star tolerance; exact on the reference's pinned examples).
+// Products and sums are explicit __dmul_rn / __dadd_rn (no FMA contraction), as in the
+// reference build (pkg/setup.py:4-13).
+#include <algorithm>
+
+#include "tk_host.h"
+#include "tk_common.cuh"
+
+namespace tk {
+
+namespace {
+constexpr int kDotThreads = 256;
+constexpr int kDotUnroll = 4;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) s_warp[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;  // valid in warp 0
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double* __restrict__ x,
+                                                                  const double* __restrict__ y, long long n,
+                                                                  double* __restrict__ partial, int vec2) {
+  __shared__ double s_warp[kDotThreads / 32];
+  double acc = 0.0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (vec2) {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* y2 = reinterpret_cast<const double2*>(y);
+    const long long n2 = n >> 1;
+    long long i = tid;
+    for (; i + (kDotUnroll - 1) * stride < n2; i += kDotUnroll * stride) {
+      double2 a[kDotUnroll], b[kDotUnroll];
+#pragma unroll
+      for (int u = 0; u < kDotUnroll; ++u) {
+        a[u] = __ldcs(x2 + i + u * stride);
+        b[u] = __ldcs(y2 + i + u * stride);
+      }
+#pragma unroll
+      for (int u = 0; u < kDotUnroll; ++u) {
+        acc = __dadd_rn(acc, __dmul_rn(a[u].x, b[u].x));
+        acc = __dadd_rn(acc, __dmul_rn(a[u].y, b[u].y));
+      }
+    }
+    for (; i < n2; i += stride) {
+      const double2 a = __ldcs(x2 + i), b = __ldcs(y2 + i);
+      acc = __dadd_rn(acc, __dmul_rn(a.x, b.x));
+      acc = __dadd_rn(acc, __dmul_rn(a.y, b.y));
+    }
+    if ((n & 1) && tid == 0) acc = __dadd_rn(acc, __dmul_rn(x[n - 1], y[n - 1]));
+  } else {
+    for (long long i = tid; i < n; i += stride) acc = __dadd_rn(acc, __dmul_rn(x[i], y[i]));
+  }
+  const double s = block_sum(acc, s_warp);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kDotThreads) dot_final_kernel(const double* __restrict__ partial, int nblk,
+                                                                double* __restrict__ out) {
+  __shared__ double s_warp[kDotThreads / 32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc = __dadd_rn(acc, partial[i]);
+  const double s = block_sum(acc, s_warp);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// One warp per row; 128-bit loads of the row (streamed), x through the read-only path (L1
+// resident after the first rows).  The warp butterfly fixes the combine order.
+constexpr int kMvWarps = 8;
+constexpr int kMvUnroll = 8;
+
+__global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __restrict__ a, long long rows,
+                                                                long long cols, const double* __restrict__ x,
+                                                                double* __restrict__ y, int vec2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row = (long long)blockIdx.x * kMvWarps + warp;
+  if (row >= rows) return;
+  const double* ar = a + row * cols;
+  double acc = 0.0;
+  if (vec2) {
+    const double2* a2 = reinterpret_cast<const double2*>(ar);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const long long c2 = cols >> 1;
+    long long j = lane;
+    for (; j + (kMvUnroll - 1) * 32 < c2; j += kMvUnroll * 32) {
+      double2 av[kMvUnroll], xv[kMvUnroll];
+#pragma unroll
+      for (int u = 0; u < kMvUnroll; ++u) {
+        av[u] = __ldcs(a2 + j + u * 32);
+        xv[u] = __ldg(x2 + j + u * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < kMvUnroll; ++u) {
+        acc = __dadd_rn(acc, __dmul_rn(av[u].x, xv[u].x));
+        acc = __dadd_rn(acc, __dmul_rn(av[u].y, xv[u].y));
+      }
+    }
+    for (; j < c2; j += 32) {
+      const double2 av = __ldcs(a2 + j), xv = __ldg(x2 + j);
+      acc = __dadd_rn(acc, __dmul_rn(av.x, xv.x));
+      acc = __dadd_rn(acc, __dmul_rn(av.y, xv.y));
+    }
+    if ((cols & 1) && lane == 0) acc = __dadd_rn(acc, __dmul_rn(ar[cols - 1], x[cols - 1]));
+  } else {
+    for (long long j = lane; j < cols; j += 32) acc = __dadd_rn(acc, __dmul_rn(ar[j], __ldg(x + j)));
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int dot_blocks(long long n) {
+  const long long want = (n + 2LL * kDotThreads * kDotUnroll - 1) / (2LL * kDotThreads * kDotUnroll);
+  return (int)std::max(1LL, std::min(want, (long long)num_sms() * 8));
+}
+
+int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStream_t st) {
+  if (n == 0) {
+    TK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return TK_OK;
+  }
+  const int nblk = dot_blocks(n);
+  DevBuf part;
+  if (int rc = part.alloc((size_t)nblk * sizeof(double), st)) return rc;
+  const int vec2 = al16(x) && al16(y);
+  ktimer_begin(st);
+  dot_partial_kernel<<<nblk, kDotThreads, 0, st>>>(x, y, n, part.as<double>(), vec2);
+  dot_final_kernel<<<1, kDotThreads, 0, st>>>(part.as<double>(), nblk, out);
+  ktimer_end(st);
+  count_launch(2);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+int matvec_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, cudaStream_t st) {
+  if (rows == 0) return TK_OK;
+  const int vec2 = al16(a) && al16(x) && (cols % 2 == 0);
+  const long long nblk = (rows + kMvWarps - 1) / kMvWarps;
+  ktimer_begin(st);
+  matvec_kernel<<<(unsigned)nblk, kMvWarps * 32, 0, st>>>(a, rows, cols, x, y, vec2);
+  ktimer_end(st);
+  count_launch();
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+}  // namespace tk

@@ -1,0 +1,83 @@
+// tk_host.h -- internal host-side API shared by the translation units of libtk_b200.so.
+// (The public, stable surface is include/tk_b200.h.)
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tk_b200.h"
+
+namespace tk {
+
+// Thread-local last-error message, returned by tk_last_error().
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define TK_CUDA(expr)                                         \
+  do {                                                        \
+    cudaError_t tk_e_ = (expr);                               \
+    if (tk_e_ != cudaSuccess) return cuda_fail(tk_e_, #expr); \
+  } while (0)
+
+// Stream-ordered scratch from the device's default memory pool.  The pool keeps freed
+// blocks (release threshold raised at first use), so steady-state calls allocate nothing.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_), st_(o.st_) { o.ptr_ = nullptr; o.bytes_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      ptr_ = o.ptr_; bytes_ = o.bytes_; st_ = o.st_;
+      o.ptr_ = nullptr; o.bytes_ = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  int alloc(size_t bytes, cudaStream_t st);
+  void reset();
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr_); }
+  void* get() const { return ptr_; }
+  size_t size() const { return bytes_; }
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+  cudaStream_t st_ = nullptr;
+};
+
+// Small per-thread pinned host block used to read back per-call counters.
+void* pinned_scratch(size_t bytes);
+
+int num_sms();
+void prepare_pool();
+
+// Instrumentation read by bench.py: CUDA events around the primary kernel of the last call
+// (recorded on the launching stream) and a count of this library's kernel launches.
+void ktimer_begin(cudaStream_t st);
+void ktimer_end(cudaStream_t st);
+void count_launch(int n = 1);
+
+// sparse-result TTV on device-resident SoA data (cols[m] device pointers, m < d).
+int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                      const double* x, int64_t nx, int k, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
+                      cudaStream_t st, bool keep_zeros = false);
+
+// dense-result multi-vector TTV (every mode except `keep` contracted).
+int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                     int keep, const double* const* vecs, double* out, cudaStream_t st);
+
+// row-major (nnz, d) -> SoA columns with the given pitch (elements)
+int aos_to_soa(int64_t nnz, int d, const int64_t* aos, int64_t* soa, int64_t pitch, cudaStream_t st);
+
+int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStream_t st);
+int matvec_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, cudaStream_t st);
+
+}  // namespace tk

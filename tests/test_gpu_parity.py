@@ -1,0 +1,301 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle and the
+reference's golden vectors.  Bar: coordinates bit-exact; TTV values bit-exact (serial
+in-group folds, the reference's exact operation order); dot / matvec / dense
+multi-vector TTV within 1e-12 relative (north-star tolerance, written per test)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import ttv_cases
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12  # north-star FP64 tolerance for tree-order reductions
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2510_01495_b200 import _lib, backend
+    assert _lib.device_count() > 0, "no CUDA device visible"
+    return backend.kernels()
+
+
+def assert_ttv_equal(got, exp, name=""):
+    s, v, sh = got
+    assert tuple(sh) == tuple(exp[2]), name
+    assert np.asarray(s).shape == np.asarray(exp[0]).shape, name
+    assert np.asarray(s).tobytes() == np.asarray(exp[0]).tobytes(), name
+    assert np.asarray(v).tobytes() == np.asarray(exp[1]).tobytes(), name
+
+
+def test_golden_ttv_cases_bit_exact(K, golden_small, golden_hashes):
+    from paper_2510_01495_b200 import errors
+    for name, subs, vals, shape, x, k, err, exp in ttv_cases(golden_small, golden_hashes):
+        if err:
+            with pytest.raises(getattr(errors, err)):
+                K.ttv_raw(subs, vals, shape, x, k)
+            continue
+        assert_ttv_equal(K.ttv_raw(subs, vals, shape, x, k), exp, name)
+
+
+def test_golden_dense_cases(K, golden_small, golden_hashes):
+    for i in range(golden_hashes["dense_cases"]):
+        a, x, y = golden_small[f"d{i}_a"], golden_small[f"d{i}_x"], golden_small[f"d{i}_y"]
+        np.testing.assert_allclose(K.matvec(a, x), golden_small[f"d{i}_mv"], rtol=REL, atol=0)
+        np.testing.assert_allclose(K.dot(x, y), golden_small[f"d{i}_dot"], rtol=REL, atol=0)
+
+
+def test_dense_pinned_examples_exact():
+    import paper_2510_01495_b200 as tk
+    assert tk.dot([1.0, 2.0, 3.0], [4.0, 5.0, 6.0]) == 32.0
+    assert tk.dot([], []) == 0.0
+    assert tk.dot([0.0, 0.0, 0.0], [5.0, 5.0, 5.0]) == 0.0
+    y = np.random.default_rng(3).random(6)
+    for i in range(6):
+        e = np.zeros(6)
+        e[i] = 1.0
+        assert np.float64(tk.dot(e, y)).tobytes() == np.float64(y[i]).tobytes()
+    assert np.array_equal(tk.matvec(np.eye(2), [3.0, 7.0]), [3.0, 7.0])
+    assert np.array_equal(tk.matvec([[1.0, 2.0], [3.0, 4.0]], [1.0, 1.0]), [3.0, 7.0])
+    assert tk.matvec(np.zeros((0, 3)), [1.0, 1.0, 1.0]).shape == (0,)
+    assert np.array_equal(tk.matvec(np.zeros((2, 0)), []), [0.0, 0.0])
+    assert tk.dot([1, 2], [3, 4]) == 11.0
+
+
+def test_config1_dot_full_size(K, oracle, golden_hashes):
+    from paper_2510_01495_b200 import synth
+    ops = synth.host_operands(1)
+    ref = float.fromhex(golden_hashes["cfg1"]["dot_hex"])
+    got = K.dot(ops["x"], ops["y"])
+    assert abs(got - ref) <= REL * abs(ref)
+    for n in (1, 2, 3, 17, 1023, 4097, 100001):
+        x, y = np.random.default_rng(n).random(n), np.random.default_rng(n + 1).random(n)
+        r = oracle.dot(x, y)
+        assert abs(K.dot(x, y) - r) <= REL * abs(r)
+    # unaligned views take the scalar path
+    x = np.random.default_rng(5).random(1001)
+    assert abs(K.dot(x[1:], x[:-1]) - oracle.dot(x[1:], x[:-1])) <= REL * oracle.dot(x[1:], x[:-1])
+
+
+def test_config2_matvec_full_size(K, oracle):
+    from paper_2510_01495_b200 import synth
+    ops = synth.host_operands(2)
+    ref = oracle.matvec(ops["a"], ops["x"])
+    np.testing.assert_allclose(K.matvec(ops["a"], ops["x"]), ref, rtol=REL, atol=0)
+    for rows, cols in ((1, 1), (7, 3), (33, 65), (100, 4097), (3000, 1)):
+        rng = np.random.default_rng(rows * 7 + cols)
+        a, x = rng.random((rows, cols)), rng.random(cols)
+        np.testing.assert_allclose(K.matvec(a, x), oracle.matvec(a, x), rtol=REL, atol=0)
+
+
+def test_config3_full_size_matches_reference_hashes(K, golden_hashes):
+    from paper_2510_01495_b200 import synth
+    ops = synth.host_operands(3)
+    t, g = ops["tensor"], golden_hashes["cfg3"]
+    s, v, sh = K.ttv_raw(t.subs, t.vals, t.shape, ops["x"], ops["k0"])
+    assert len(v) == g["u"] and sha(s) == g["out_subs"] and sha(v) == g["out_vals"]
+    assert list(sh) == g["out_shape"]
+    g1 = golden_hashes["cfg3_k1"]  # the paper's own middle-mode protocol: the sort path
+    s, v, _ = K.ttv_raw(t.subs, t.vals, t.shape, ops["x"], 1)
+    assert len(v) == g1["u"] and sha(s) == g1["out_subs"] and sha(v) == g1["out_vals"]
+
+
+def _random_tensor(rng, shape, nnz, normal=True, zipf=None):
+    if zipf:
+        cols = [np.minimum(rng.zipf(zipf, size=3 * nnz) - 1, n - 1) for n in shape]
+        lin = np.unique(np.ravel_multi_index(cols, shape))[:nnz]
+    else:
+        lin = np.unique(rng.integers(0, int(np.prod(shape)), size=nnz))
+    subs = np.column_stack(np.unravel_index(lin, shape)).astype(np.int64)
+    vals = rng.standard_normal(lin.size) if normal else rng.random(lin.size)
+    return subs, vals
+
+
+@pytest.mark.parametrize("shape,nnz,zipf", [
+    ((50, 40, 30), 20000, None),
+    ((2000, 300, 700), 300000, None),
+    ((3000, 2000, 5000), 400000, 1.2),      # skewed: long groups, spills across tiles
+    ((7, 9), 50, None),                      # order 2
+    ((6, 5, 4, 3, 7), 2000, None),           # order 5
+    ((3, 3, 3, 3, 3, 3, 3, 3, 3), 4000, None),  # order 9: runtime-width key kernels
+])
+def test_random_all_modes_bit_exact(K, oracle, shape, nnz, zipf):
+    rng = np.random.default_rng(sum(shape) + nnz)
+    subs, vals = _random_tensor(rng, shape, nnz, zipf=zipf)
+    for k in range(len(shape)):
+        x = rng.standard_normal(shape[k])
+        assert_ttv_equal(K.ttv_raw(subs, vals, shape, x, k), oracle.ttv_raw(subs, vals, shape, x, k),
+                         f"{shape} k={k}")
+
+
+def test_single_group_spanning_many_tiles(K, oracle):
+    # one kept key, 300k rows: the CTA-cooperative spill fold over ~150 tiles
+    n = 300000
+    subs = np.column_stack([np.zeros(n), np.zeros(n), np.arange(n)]).astype(np.int64)
+    vals = np.random.default_rng(11).standard_normal(n)
+    x = np.random.default_rng(12).standard_normal(n)
+    assert_ttv_equal(K.ttv_raw(subs, vals, (1, 1, n), x, 2), oracle.ttv_raw(subs, vals, (1, 1, n), x, 2))
+    # groups of length 2047..2049 straddling tile edges
+    lens = np.tile([2047, 2048, 2049, 1, 4096], 20)
+    i0 = np.repeat(np.arange(lens.size), lens)
+    i2 = np.concatenate([np.arange(L) for L in lens])
+    subs = np.column_stack([i0, np.zeros_like(i0), i2]).astype(np.int64)
+    vals = np.random.default_rng(13).standard_normal(i0.size)
+    shape = (lens.size, 1, 4096)
+    x = np.random.default_rng(14).standard_normal(4096)
+    assert_ttv_equal(K.ttv_raw(subs, vals, shape, x, 2), oracle.ttv_raw(subs, vals, shape, x, 2))
+
+
+def test_exact_zero_groups_compacted(K, oracle):
+    # +v / -v pairs in the same group cancel exactly; scattered through many tiles
+    rng = np.random.default_rng(21)
+    g = 100000
+    base = rng.standard_normal(g)
+    cancel = rng.random(g) < 0.3
+    i0 = np.repeat(np.arange(g), 2)
+    i2 = np.tile([0, 1], g)
+    vals = np.empty(2 * g)
+    vals[0::2] = base
+    vals[1::2] = np.where(cancel, -base, rng.standard_normal(g))
+    subs = np.column_stack([i0, np.zeros_like(i0), i2]).astype(np.int64)
+    x = np.ones(2)
+    got = K.ttv_raw(subs, vals, (g, 1, 2), x, 2)
+    exp = oracle.ttv_raw(subs, vals, (g, 1, 2), x, 2)
+    assert len(exp[1]) == g - cancel.sum()
+    assert_ttv_equal(got, exp)
+
+
+def test_unsorted_and_duplicate_raw_buffers(K, oracle):
+    rng = np.random.default_rng(31)
+    subs = rng.integers(0, 40, size=(50000, 3)).astype(np.int64)
+    vals = rng.standard_normal(50000)
+    for k in range(3):
+        x = rng.standard_normal(40)
+        assert_ttv_equal(K.ttv_raw(subs, vals, (40, 40, 40), x, k), oracle.ttv_raw(subs, vals, (40, 40, 40), x, k))
+
+
+def test_garbage_kept_indices_do_not_crash_and_match(K, oracle):
+    from paper_2510_01495_b200 import errors
+    rng = np.random.default_rng(41)
+    subs = rng.integers(-10**12, 10**12, size=(5000, 3)).astype(np.int64)
+    subs[:, 2] = rng.integers(0, 4, size=5000)
+    vals = rng.standard_normal(5000)
+    x = rng.standard_normal(4)
+    assert_ttv_equal(K.ttv_raw(subs, vals, (4, 4, 4), x, 2), oracle.ttv_raw(subs, vals, (4, 4, 4), x, 2))
+    subs[17, 2] = 4  # contracted-mode index outside x: must raise, never read out of bounds
+    with pytest.raises(errors.DimensionError, match="index out of range"):
+        K.ttv_raw(subs, vals, (4, 4, 4), x, 2)
+
+
+def test_public_api_and_canonicalisation_on_device():
+    import paper_2510_01495_b200 as tk
+    t = tk.SparseCooTensor([[1, 1], [0, 0], [1, 1], [0, 1]], [2.0, 1.0, 3.0, 0.0], (2, 2))
+    assert t.subs.tolist() == [[0, 0], [1, 1]] and t.vals.tolist() == [1.0, 5.0]
+    assert tk.SparseCooTensor([[0, 0], [0, 0]], [1.5, -1.5], (2, 2)).nnz == 0
+    res = tk.ttv(tk.SparseCooTensor([[0, 0, 0], [0, 1, 0]], [2.0, 3.0], (2, 2, 2)), [10.0, 100.0], 1)
+    assert isinstance(res, tk.TtvRawResult)
+    assert res.to_tensor() == tk.SparseCooTensor([[0, 0]], [320.0], (2, 2))
+    u, s = tk.unique_rows_accumulate([[0, 0], [0, 0], [1, 2]], [1.0, 2.0, 3.0])
+    assert u.tolist() == [[0, 0], [1, 2]] and s.tolist() == [3.0, 3.0]
+    _, s = tk.unique_rows_accumulate([[0], [0], [0]], [1e16, 1.0, -1e16])
+    assert s[0] == ((1e16 + 1.0) + -1e16)
+    u, s = tk.unique_rows_accumulate([], [])
+    assert u.shape[0] == 0 and s.shape == (0,)
+    keys = np.array([[3, 1], [0, 2], [2, 0]])
+    w = np.array([0.1, 0.2, 0.3])
+    u, s = tk.unique_rows_accumulate(keys, w)
+    assert u.tolist() == [[0, 2], [2, 0], [3, 1]] and s.tolist() == [0.2, 0.3, 0.1]
+
+
+def test_unique_rows_accumulate_matches_reference_pykernels_semantics(oracle):
+    import paper_2510_01495_b200 as tk
+    rng = np.random.default_rng(51)
+    for _ in range(10):
+        n = int(rng.integers(1, 3000))
+        keys = rng.integers(-3, 4, size=(n, 3))
+        w = rng.standard_normal(n)
+        u, s = tk.unique_rows_accumulate(keys, w)
+        # oracle: TTV with an appended singleton contracted mode keeps the order, but drops
+        # zero sums; compare on the nonzero groups and the full key set
+        order = np.lexsort(keys.T[::-1])
+        ks = keys[order]
+        first = np.ones(n, dtype=bool)
+        first[1:] = (ks[1:] != ks[:-1]).any(axis=1)
+        assert np.array_equal(u, ks[first])
+        exp = []
+        for i in np.flatnonzero(first):
+            j = i
+            acc = w[order[i]]
+            j += 1
+            while j < n and not first[j]:
+                acc += w[order[j]]
+                j += 1
+            exp.append(acc)
+        assert np.asarray(exp).tobytes() == s.tobytes()
+
+
+def test_timed_entry_points(K):
+    x, y = np.random.default_rng(1).random(1000), np.random.default_rng(2).random(1000)
+    v, el = K.dot_timed(x, y)
+    assert v == K.dot(x, y) and el > 0
+    a = np.random.default_rng(3).random((40, 25))
+    out, el = K.matvec_timed(a, y[:25])
+    assert out.tobytes() == K.matvec(a, y[:25]).tobytes() and el > 0
+    import paper_2510_01495_b200 as tk
+    t = tk.gen_sparse3(tk.GenSpec(4, "sparse3", (15, 15, 15), 0.1))
+    (s, v, sh), el = K.ttv_timed(t.subs, t.vals, t.shape, x[:15], 1)
+    s2, v2, sh2 = K.ttv_raw(t.subs, t.vals, t.shape, x[:15], 1)
+    assert s.tobytes() == s2.tobytes() and v.tobytes() == v2.tobytes() and sh == sh2 and el > 0
+    # release_gil positional flag accepted (BoundKernelSet passes it positionally)
+    assert K.dot(x, y, True) == K.dot(x, y)
+
+
+def test_device_generator_and_device_ttv(oracle):
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (20000, 5000, 1000)
+    t = DeviceCoo.generate(shape, 2_000_000, zipf_s=1.2, normal_vals=True, seed=99)
+    subs, vals = t.to_host()
+    assert subs.shape == (2_000_000, 3) and (vals != 0).all()
+    lin = np.ravel_multi_index(subs.T, shape)
+    assert (np.diff(lin) > 0).all()  # canonical: sorted, unique
+    t2 = DeviceCoo.generate(shape, 2_000_000, zipf_s=1.2, normal_vals=True, seed=99)
+    assert torch.equal(t2.cols[0], t.cols[0]) and torch.equal(t2.vals, t.vals)  # deterministic
+    x = uniform_vector(shape[2], 7)
+    u, os_, ov = t.ttv(x, 2)
+    s, v, _ = oracle.ttv_raw(subs, vals, shape, x.cpu().numpy(), 2)
+    assert u == len(v)
+    assert os_[:u].cpu().numpy().tobytes() == s.tobytes()
+    assert ov[:u].cpu().numpy().tobytes() == v.tobytes()
+
+
+def test_dense_multi_vector_ttv(oracle):
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (2000, 2000, 2000, 2000)
+    t = DeviceCoo.generate(shape, 1_000_000, seed=5)
+    vecs = {m: uniform_vector(shape[m], 100 + m) for m in (1, 2, 3)}
+    out = t.ttv_dense(vecs, 0).cpu().numpy()
+    subs, vals = t.to_host()
+    ref = oracle.ttv_multi_dense(subs, vals, shape, {m: v.cpu().numpy() for m, v in vecs.items()}, 0)
+    nz = ref != 0
+    assert np.array_equal(out != 0, nz)
+    assert np.max(np.abs(out[nz] - ref[nz]) / np.abs(ref[nz])) <= REL
+    # keep != 0: the chained device path, bit-exact with the chained oracle
+    vecs0 = {m: uniform_vector(shape[m], 200 + m) for m in (0, 2, 3)}
+    out1 = t.ttv_dense(vecs0, 1).cpu().numpy()
+    ref1 = oracle.ttv_multi_dense(subs, vals, shape, {m: v.cpu().numpy() for m, v in vecs0.items()}, 1)
+    assert out1.tobytes() == ref1.tobytes()
+    # a small-valued case across many tiles with long runs
+    small = DeviceCoo.generate((4, 50, 60, 70), 200000, seed=6)
+    vv = {m: uniform_vector(small.shape[m], 300 + m) for m in (1, 2, 3)}
+    o = small.ttv_dense(vv, 0).cpu().numpy()
+    s2, v2 = small.to_host()
+    r = oracle.ttv_multi_dense(s2, v2, small.shape, {m: v.cpu().numpy() for m, v in vv.items()}, 0)
+    assert np.max(np.abs(o - r) / np.abs(r)) <= REL

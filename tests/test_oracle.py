@@ -1,0 +1,105 @@
+"""Pin the CPU oracle (oracle/tk_oracle.c) against the reference's own outputs.
+
+The golden fixtures were produced by running the reference (tests/golden/make_golden.py);
+the oracle must reproduce them bit for bit before any GPU parity claim rests on it.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import ttv_cases
+from paper_2510_01495_b200 import errors, synth
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_oracle_ttv_matches_reference_golden(oracle, golden_small, golden_hashes):
+    n = 0
+    for name, subs, vals, shape, x, k, err, exp in ttv_cases(golden_small, golden_hashes):
+        if err:
+            with pytest.raises(getattr(errors, err)):
+                oracle.ttv_raw(subs, vals, shape, x, k)
+            continue
+        s, v, sh = oracle.ttv_raw(subs, vals, shape, x, k)
+        assert s.tobytes() == exp[0].tobytes(), name
+        assert v.tobytes() == exp[1].tobytes(), name
+        assert sh == exp[2], name
+        n += 1
+    assert n >= 100
+
+
+def test_oracle_dense_matches_reference_golden(oracle, golden_small, golden_hashes):
+    for i in range(golden_hashes["dense_cases"]):
+        a, x, y = golden_small[f"d{i}_a"], golden_small[f"d{i}_x"], golden_small[f"d{i}_y"]
+        assert oracle.matvec(a, x).tobytes() == golden_small[f"d{i}_mv"].tobytes()
+        assert np.float64(oracle.dot(x, y)).tobytes() == golden_small[f"d{i}_dot"].tobytes()
+
+
+def test_oracle_errors_mirror_reference(oracle):
+    x = np.ones(3)
+    subs = np.zeros((1, 3), dtype=np.int64)
+    with pytest.raises(errors.ModeError):
+        oracle.ttv_raw(subs, [1.0], (3, 3, 3), x, 3)
+    with pytest.raises(errors.DimensionError):
+        oracle.ttv_raw(subs, [1.0], (3, 4, 3), x, 1)
+    with pytest.raises(errors.OrderError):
+        oracle.ttv_raw(np.zeros((1, 1), dtype=np.int64), [1.0], (3,), x, 0)
+    with pytest.raises(errors.DimensionError):
+        oracle.dot([1.0, 2.0], [1.0])
+
+
+def test_host_generator_and_oracle_pin_config1(oracle, golden_hashes):
+    ops = synth.host_operands(1)
+    g = golden_hashes["cfg1"]
+    assert sha(ops["x"]) == g["x"] and sha(ops["y"]) == g["y"]
+    assert float(oracle.dot(ops["x"], ops["y"])).hex() == g["dot_hex"]
+
+
+def test_host_generator_and_oracle_pin_config2(oracle, golden_hashes):
+    ops = synth.host_operands(2)
+    g = golden_hashes["cfg2"]
+    assert sha(ops["a"]) == g["a"] and sha(ops["x"]) == g["x"]
+    assert sha(oracle.matvec(ops["a"], ops["x"])) == g["y"]
+
+
+def test_host_generator_and_oracle_pin_config3(oracle, golden_hashes):
+    ops = synth.host_operands(3)
+    t, g = ops["tensor"], golden_hashes["cfg3"]
+    assert t.nnz == g["nnz"] and sha(t.subs) == g["subs"] and sha(t.vals) == g["vals"]
+    assert sha(ops["x"]) == g["x"] and ops["k0"] == g["k0"]
+    s, v, sh = oracle.ttv_raw(t.subs, t.vals, t.shape, ops["x"], ops["k0"])
+    assert len(v) == g["u"] and sha(s) == g["out_subs"] and sha(v) == g["out_vals"]
+    assert list(sh) == g["out_shape"]
+    g1 = golden_hashes["cfg3_k1"]
+    s, v, _ = oracle.ttv_raw(t.subs, t.vals, t.shape, ops["x"], 1)
+    assert len(v) == g1["u"] and sha(s) == g1["out_subs"] and sha(v) == g1["out_vals"]
+
+
+def test_multi_vector_oracle_against_fused_restatement(oracle):
+    # chained ttv vs bincount of the fully scaled values: <= 1e-12 relative
+    rng = np.random.default_rng(7)
+    shape = (50, 40, 30, 20)
+    lin = np.unique(rng.integers(0, int(np.prod(shape)), size=20000))
+    subs = np.column_stack(np.unravel_index(lin, shape)).astype(np.int64)
+    vals = rng.random(lin.size)
+    vecs = {m: rng.random(shape[m]) for m in (1, 2, 3)}
+    got = oracle.ttv_multi_dense(subs, vals, shape, vecs, 0)
+    w = vals * vecs[3][subs[:, 3]] * vecs[2][subs[:, 2]] * vecs[1][subs[:, 1]]
+    ref = np.bincount(subs[:, 0], weights=w, minlength=shape[0])
+    assert np.allclose(got, ref, rtol=1e-12, atol=0)
+
+
+def test_reference_extension_agrees_when_built(oracle, golden_small, golden_hashes):
+    ck = oracle.reference_module()
+    if ck is None:
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    for name, subs, vals, shape, x, k, err, exp in ttv_cases(golden_small, golden_hashes):
+        if err:
+            continue
+        s, v, sh = ck.ttv_raw(np.ascontiguousarray(subs), vals, shape, x, k)
+        assert np.asarray(s).tobytes() == exp[0].tobytes(), name
+        assert np.asarray(v).tobytes() == exp[1].tobytes(), name
