@@ -14,6 +14,8 @@
 //             ordered fix-up for runs that cross tiles; chained single-mode TTV otherwise.
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -346,12 +348,18 @@ __global__ void dense_fixup_kernel(long long ntiles, const double* __restrict__ 
 
 namespace {
 
+// Opt a kernel in to >48 KB of dynamic shared memory, once per (kernel, device).
 template <class K>
 void set_smem_once(K kernel, size_t bytes) {
-  static size_t set_bytes = 0;  // one static per kernel instantiation
-  if (bytes > set_bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{reinterpret_cast<const void*>(kernel), dev}];
+  if (bytes > have) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    set_bytes = bytes;
+    have = bytes;
   }
 }
 
