@@ -28,6 +28,10 @@ struct Counters {
   unsigned long long zeros;      // groups whose serial sum is exactly 0.0
   unsigned int flags;            // kFlag* bits
   unsigned int tile_ticket;      // dynamic tile ids (in launch order) for look-back
+  unsigned long long q_head;     // chain-job queue: next ticket handed to a chain warp
+  unsigned long long q_tail;     // chain-job queue: jobs pushed so far
+  unsigned int streamers_done;   // CTAs whose streamer warps have finished
+  unsigned int pad_;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

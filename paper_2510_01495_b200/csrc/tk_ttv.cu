@@ -23,6 +23,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "tk_host.h"
+#include "tk_stream.cuh"
 #include "tk_ttv_kernels.cuh"
 
 namespace tk {
@@ -371,55 +372,67 @@ int grid_for(long long n, int per_thread = 4) {
   return (int)std::max(1LL, std::min(want, cap));
 }
 
-template <int SRC, int NK, int kItems>
-int launch_seg_t(SegParams& p, cudaStream_t st) {
-  constexpr int TILE = SegTile<kItems>::kTile;
+template <int SRC, int NK>
+int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
+  constexpr int TILE = NK > 0 ? 1024 : 512;
+  constexpr int HALO = NK > 0 ? 64 : 32;
+  constexpr int STAGES = NK > 0 ? 3 : 2;
+  constexpr int ROWS = TILE + HALO;
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
-  const size_t smem = (size_t)(nk + 1 + (SRC == kSrcRaw ? 1 : 0)) * TILE * 8;
-  auto kern = seg_ttv_kernel<SRC, NK, kItems>;
+  const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
+  const size_t smem = ((size_t)ncol * ROWS + 2 * nk) * 8 * STAGES + (size_t)kChainWarps * kChunk * 8;
+  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES>;
   set_smem_once(kern, smem);
+  int per_sm = 0;
+  TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));
+  if (per_sm < 1) return fail(TK_EARG, "ttv: stream kernel does not fit on an SM");
   const long long ntiles = (p.n + TILE - 1) / TILE;
+  const long long job_cap = ntiles + p.n / (kShort + 1) + 1;
+  // scratch: look-back status | counters | job ready flags (all zeroed) | jobs
+  const size_t status_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
+  const size_t ready_b = ((size_t)job_cap * 4 + 255) & ~size_t(255);
+  DevBuf scratch;
+  if (int rc = scratch.alloc(status_b + 256 + ready_b + (size_t)job_cap * sizeof(StreamJob), st)) return rc;
+  char* b = scratch.as<char>();
+  p.status = reinterpret_cast<unsigned long long*>(b);
+  p.ctr = reinterpret_cast<Counters*>(b + status_b);
+  StreamParams sp{};
+  sp.s = p;
+  sp.job_ready = reinterpret_cast<unsigned int*>(b + status_b + 256);
+  sp.jobs = reinterpret_cast<StreamJob*>(b + status_b + 256 + ready_b);
+  sp.job_cap = job_cap;
+  sp.ntiles = ntiles;
+  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256 + ready_b, st));
+  const unsigned grid = (unsigned)(per_sm * num_sms());
+  void* args[] = {&sp};
   ktimer_begin(st);
-  kern<<<(unsigned)ntiles, 256, smem, st>>>(p);
+  TK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kStreamThreads), args, smem, st));
   ktimer_end(st);
   count_launch();
-  TK_CUDA(cudaGetLastError());
+  TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
   return TK_OK;
 }
 
 template <int SRC>
-int launch_seg(SegParams& p, cudaStream_t st) {
+int launch_stream(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
-  if (nk <= 4) {
-    switch (nk) {
-      case 1: return launch_seg_t<SRC, 1, 8>(p, st);
-      case 2: return launch_seg_t<SRC, 2, 8>(p, st);
-      case 3: return launch_seg_t<SRC, 3, 8>(p, st);
-      default: return launch_seg_t<SRC, 0, 8>(p, st);
-    }
+  switch (nk) {
+    case 1: return launch_stream_t<SRC, 1>(p, st, host_ctr);
+    case 2: return launch_stream_t<SRC, 2>(p, st, host_ctr);
+    case 3: return launch_stream_t<SRC, 3>(p, st, host_ctr);
+    default: return launch_stream_t<SRC, 0>(p, st, host_ctr);
   }
-  return launch_seg_t<SRC, 0, 4>(p, st);
 }
 
-long long seg_tiles(int nk, int src, long long n) {
-  const int tile = (src == kSrcLinKey || nk <= 4) ? 2048 : 1024;
-  return (n + tile - 1) / tile;
-}
-
-// Run one segmented pass over a sorted stream; returns groups/zeros/flags.
+// Run one segmented pass over a sorted stream; returns groups/zeros/flags in host_ctr.
 int run_seg(int src, SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  const long long ntiles = seg_tiles(p.nk, src, p.n);
-  DevBuf scratch;
-  const size_t status_bytes = (size_t)ntiles * 8;
-  if (int rc = scratch.alloc(status_bytes + 256, st)) return rc;
-  p.status = scratch.as<unsigned long long>();
-  p.ctr = reinterpret_cast<Counters*>(scratch.as<char>() + ((status_bytes + 127) & ~size_t(127)));
-  TK_CUDA(cudaMemsetAsync(scratch.get(), 0, scratch.size(), st));
-  int rc = src == kSrcRaw ? launch_seg<kSrcRaw>(p, st) : src == kSrcKeysW ? launch_seg<kSrcKeysW>(p, st)
-                                                                          : launch_seg<kSrcLinKey>(p, st);
+  Counters* hc = static_cast<Counters*>(pinned_scratch(sizeof(Counters)));
+  int rc = src == kSrcRaw     ? launch_stream<kSrcRaw>(p, st, hc)
+           : src == kSrcKeysW ? launch_stream<kSrcKeysW>(p, st, hc)
+                              : launch_stream<kSrcLinKey>(p, st, hc);
   if (rc) return rc;
-  TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaStreamSynchronize(st));
+  *host_ctr = *hc;
   return TK_OK;
 }
 
