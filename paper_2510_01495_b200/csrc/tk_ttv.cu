@@ -372,37 +372,60 @@ int grid_for(long long n, int per_thread = 4) {
   return (int)std::max(1LL, std::min(want, cap));
 }
 
+// Persistent, self-cleaning job queue per device (all-zero between calls: every pushed job
+// is consumed exactly once and its slot cleared by the consumer).  Grow-only.
+int stream_jobs(long long cap, StreamJob** out) {
+  static std::mutex mu;
+  static StreamJob* buf[64] = {};
+  static long long have[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cap > have[dev]) {
+    if (buf[dev]) TK_CUDA(cudaFree(buf[dev]));
+    buf[dev] = nullptr;
+    have[dev] = 0;
+    const long long want = std::max(cap, have[dev] * 2);
+    TK_CUDA(cudaMalloc(&buf[dev], (size_t)want * sizeof(StreamJob)));
+    TK_CUDA(cudaMemset(buf[dev], 0, (size_t)want * sizeof(StreamJob)));
+    have[dev] = want;
+  }
+  *out = buf[dev];
+  return TK_OK;
+}
+
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   constexpr int TILE = NK > 0 ? 1024 : 512;
-  constexpr int HALO = NK > 0 ? 64 : 32;
-  constexpr int STAGES = NK > 0 ? 3 : 2;
-  constexpr int ROWS = TILE + HALO;
+  constexpr int HALO = 32;
+  constexpr int STAGES = 2;
+  constexpr int MINB = NK > 0 ? 2 : 1;
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
-  const size_t smem = ((size_t)ncol * ROWS + 2 * nk) * 8 * STAGES + (size_t)kChainWarps * kChunk * 8;
-  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES>;
+  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES>(ncol, nk);
+  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, MINB>;
   set_smem_once(kern, smem);
   int per_sm = 0;
   TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));
   if (per_sm < 1) return fail(TK_EARG, "ttv: stream kernel does not fit on an SM");
   const long long ntiles = (p.n + TILE - 1) / TILE;
-  const long long job_cap = ntiles + p.n / (kShort + 1) + 1;
-  // scratch: look-back status | counters | job ready flags (all zeroed) | jobs
+  // at most one open group per tile plus TILE/(kShort+1) long closed groups per tile
+  const long long job_cap = ntiles * (1 + TILE / (kShort + 1)) + 1;
+  StreamJob* jobs = nullptr;
+  if (int rc = stream_jobs(job_cap, &jobs)) return rc;
+  // scratch: look-back status | counters (zeroed per call)
   const size_t status_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
-  const size_t ready_b = ((size_t)job_cap * 4 + 255) & ~size_t(255);
   DevBuf scratch;
-  if (int rc = scratch.alloc(status_b + 256 + ready_b + (size_t)job_cap * sizeof(StreamJob), st)) return rc;
+  if (int rc = scratch.alloc(status_b + 256, st)) return rc;
   char* b = scratch.as<char>();
   p.status = reinterpret_cast<unsigned long long*>(b);
   p.ctr = reinterpret_cast<Counters*>(b + status_b);
   StreamParams sp{};
   sp.s = p;
-  sp.job_ready = reinterpret_cast<unsigned int*>(b + status_b + 256);
-  sp.jobs = reinterpret_cast<StreamJob*>(b + status_b + 256 + ready_b);
-  sp.job_cap = job_cap;
+  sp.jobs = jobs;
   sp.ntiles = ntiles;
-  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256 + ready_b, st));
+  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
   const unsigned grid = (unsigned)(per_sm * num_sms());
   void* args[] = {&sp};
   ktimer_begin(st);
