@@ -1,0 +1,399 @@
+// tk_stream_kernel.cuh -- the persistent streaming TTV kernel (see tk_stream.cuh for the roles).
+//
+// Software pipeline per CTA (iteration i handles tile T_i):
+//   streamers: [wait TMA T_i] head pass T_i | folds T_i | output T_{i-LAG} | refill its stage
+//   scan warp:                 popcount T_i, publish aggregate, look-back T_i  -> arrive D_i
+// The output of T_i waits on D_i only LAG iterations later, so the look-back latency (one or
+// more L2 round trips) is hidden behind LAG tiles of streaming work.
+#pragma once
+
+#include "tk_stream.cuh"
+
+namespace tk {
+
+template <int TILE, int HALO, int STAGES, int LAG>
+constexpr size_t stream_smem_bytes(int ncol, int nk) {
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 * STAGES + (size_t)kChainWarps * kChunk * 8 +
+         (size_t)(LAG + 1) * TILE * 10;
+}
+
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int SRC, int NK, int TILE, int HALO, int STAGES, int LAG, int LBD, int MINB>
+__global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(StreamParams sp) {
+  constexpr int ROWS = TILE + HALO;
+  constexpr int WORDS = ROWS / 32;
+  constexpr int TWORDS = TILE / 32;
+  constexpr int ITER = (ROWS + 255) / 256;
+  constexpr int OWN = TILE / 256;  // rows owned per streamer thread (blocked)
+  constexpr int NB = LAG + 1;      // fold-result buffers / look-back barriers in flight
+  constexpr int NSB = kStreamWarps * 32;
+  constexpr int NSS = NSB + 32;    // streamers + scan warp
+  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE < 4096, "tile geometry");
+  static_assert(STAGES >= LAG + 2, "a stage per pending tile plus one in flight");
+  static_assert(4 + NB <= 16, "named barrier ids");
+  const SegParams& p = sp.s;
+  const int nk = seg_nk<SRC, NK>(p);
+  const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const size_t stage_words = (size_t)ncol * ROWS + 2 * nk;  // + [nk][2] previous-row words
+  long long* stage0 = reinterpret_cast<long long*>(smem_raw);
+  double* chain_buf = reinterpret_cast<double*>(stage0 + stage_words * STAGES);
+  double* s_val = chain_buf + kChainWarps * kChunk;           // [NB][TILE] folded values by local id
+  short* s_row = reinterpret_cast<short*>(s_val + NB * TILE);  // [NB][TILE] head row (-1: chain job)
+
+  __shared__ __align__(8) uint64_t s_full[STAGES];
+  __shared__ long long s_stage_tile[STAGES];
+  __shared__ int s_stage_bulk[STAGES];
+  __shared__ unsigned int s_head[WORDS];
+  __shared__ int s_wpref[TWORDS];
+  __shared__ int s_nheads[NB];
+  __shared__ unsigned long long s_base[NB];
+  __shared__ unsigned int s_flags;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&s_full[s], 1);
+    s_flags = 0;
+  }
+  __syncthreads();
+
+  if (warp <= kScanWarp) {
+    const bool scan = warp == kScanWarp;
+    auto acquire_issue = [&](int s) {  // streamer thread 0 only
+      const unsigned int t = atomicAdd(&p.ctr->tile_ticket, 1u);
+      if ((long long)t >= sp.ntiles) {
+        s_stage_tile[s] = -1;
+        return;
+      }
+      s_stage_tile[s] = t;
+      const long long start = (long long)t * TILE;
+      const long long avail = min((long long)ROWS, p.n - start);
+      long long* st = stage0 + stage_words * s;
+      const bool bulk = p.bulk_ok && avail == ROWS;
+      s_stage_bulk[s] = bulk;
+      if (!bulk) return;  // filled cooperatively by the streamers
+      const uint32_t bytes = ROWS * 8u;
+      mbar_arrive_expect_tx(&s_full[s], bytes * ncol + (start > 0 ? 16u * nk : 0u));
+      for (int c = 0; c < nk; ++c) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(st + (size_t)c * ROWS)),
+            "l"(p.key[c] + start), "r"(bytes), "r"(smem_u32(&s_full[s]))
+            : "memory");
+        if (start > 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                  smem_u32(st + (size_t)ncol * ROWS + 2 * c)),
+              "l"(p.key[c] + start - 2), "r"(smem_u32(&s_full[s]))
+              : "memory");
+      }
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(st + (size_t)nk * ROWS)),
+          "l"(p.a + start), "r"(bytes), "r"(smem_u32(&s_full[s]))
+          : "memory");
+      if constexpr (SRC == kSrcRaw)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(st + (size_t)(nk + 1) * ROWS)),
+            "l"(p.subk + start), "r"(bytes), "r"(smem_u32(&s_full[s]))
+            : "memory");
+    };
+
+    if (tid == 0)
+      for (int s = 0; s < STAGES; ++s) acquire_issue(s);
+    unsigned int phase = 0;
+    unsigned int flags = 0;
+    long long hist[LAG];
+#pragma unroll
+    for (int k = 0; k < LAG; ++k) hist[k] = -1;
+    int s = 0;
+    for (long long i = 0;; ++i) {
+      named_bar(2, NSS);  // (A) stage s descriptor visible
+      const long long tile = s_stage_tile[s];
+      const long long out_tile = hist[LAG - 1];  // tile of iteration i - LAG
+      bool any = tile >= 0 || out_tile >= 0;
+#pragma unroll
+      for (int k = LAG - 1; k > 0; --k) {
+        hist[k] = hist[k - 1];
+        any = any || hist[k] >= 0;
+      }
+      hist[0] = tile;
+      if (!any) break;
+      const int b = (int)(i % NB);
+
+      if (tile >= 0) {
+        long long* st = stage0 + stage_words * s;
+        long long* s_key = st;
+        double* s_a = reinterpret_cast<double*>(st + (size_t)nk * ROWS);
+        const long long* s_subk = st + (size_t)(nk + 1) * ROWS;
+        const long long* s_prev2 = st + (size_t)ncol * ROWS;
+        const long long start = tile * TILE;
+        const int cnt = (int)min((long long)TILE, p.n - start);
+        const int avail = (int)min((long long)ROWS, p.n - start);
+        if (!scan) {
+          if (s_stage_bulk[s]) {
+            mbar_wait(&s_full[s], (phase >> s) & 1u);
+            phase ^= 1u << s;
+          } else {
+            for (int r = tid; r < avail; r += NSB) {
+              for (int c = 0; c < nk; ++c) s_key[c * ROWS + r] = p.key[c][start + r];
+              s_a[r] = p.a[start + r];
+              if constexpr (SRC == kSrcRaw) st[(size_t)(nk + 1) * ROWS + r] = p.subk[start + r];
+            }
+            if (tid < nk && start > 0) st[(size_t)ncol * ROWS + 2 * tid + 1] = p.key[tid][start - 1];
+            named_bar(1, NSB);
+          }
+          // ---- w and head flags (striped rows: conflict-free shared memory) ----
+#pragma unroll
+          for (int j = 0; j < ITER; ++j) {
+            const int r = j * 256 + tid;
+            bool head = false;
+            if (r < avail) {
+              if constexpr (SRC == kSrcRaw) {
+                const long long idx = s_subk[r];
+                double w = 0.0;
+                if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+                else w = __dmul_rn(s_a[r], __ldg(p.x + idx));
+                s_a[r] = w;
+              }
+              int cmp = 0;
+#pragma unroll
+              for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c) {
+                if (NK == 0 && c >= nk) break;
+                const long long va = s_key[c * ROWS + r];
+                const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
+                if (va != vb) {
+                  cmp = va < vb ? -1 : 1;
+                  break;
+                }
+              }
+              if (r == 0 && start == 0) cmp = 1;
+              head = cmp != 0;
+              if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
+            }
+            const unsigned int m = __ballot_sync(0xffffffffu, head);
+            const int wi = j * 8 + warp;
+            if (lane == 0 && wi < WORDS) s_head[wi] = m;
+          }
+        }
+        named_bar(2, NSS);  // (B) heads ready
+
+        if (scan) {
+          constexpr int PL = (TWORDS + 31) / 32;
+          int cw[PL];
+          int mine = 0;
+#pragma unroll
+          for (int q = 0; q < PL; ++q) {
+            const int wi = lane * PL + q;
+            unsigned int word = 0;
+            if (wi < TWORDS && wi * 32 < cnt) {
+              word = s_head[wi];
+              if (wi * 32 + 32 > cnt) word &= (1u << (cnt - wi * 32)) - 1u;
+            }
+            cw[q] = __popc(word);
+            mine += cw[q];
+          }
+          int incl = mine;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+          }
+          int run = incl - mine;
+#pragma unroll
+          for (int q = 0; q < PL; ++q) {
+            const int wi = lane * PL + q;
+            if (wi < TWORDS) s_wpref[wi] = run;
+            run += cw[q];
+          }
+          const int agg = __shfl_sync(0xffffffffu, incl, 31);
+          if (lane == 0) s_nheads[b] = agg;
+          lookback_publish_agg<LBD>(p.status, tile, (unsigned long long)agg);
+          __syncwarp();
+          named_bar(3, NSS);  // (C) local ids ready
+          const unsigned long long excl = lookback_wide<LBD>(p.status, tile, (unsigned long long)agg);
+          if (lane == 0) {
+            s_base[b] = excl;
+            if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
+          }
+          __syncwarp();
+          named_arrive(4 + b, NSS);  // (D_i) base of tile i ready
+        } else {
+          named_bar(3, NSS);  // (C)
+          const int nheads = s_nheads[b];
+          double* vb = s_val + (size_t)b * TILE;
+          short* rb = s_row + (size_t)b * TILE;
+          const int r0 = tid * OWN;
+#pragma unroll 1
+          for (int q = 0; q < OWN; ++q) {
+            const int r = r0 + q;
+            if (r >= cnt) break;
+            const unsigned int word = s_head[r >> 5];
+            if (!((word >> (r & 31)) & 1u)) continue;
+            const int li = s_wpref[r >> 5] + __popc(word & ((1u << (r & 31)) - 1u));
+            int end = avail;
+            {
+              const int q1 = r + 1;
+              int wi = q1 >> 5;
+              unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
+              while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
+              if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
+            }
+            const bool open = end == avail && start + avail < p.n;
+            if (!open && end - r <= kShort) {
+              vb[li] = fold_run(s_a, r + 1, end, s_a[r]);
+              rb[li] = (short)r;
+            } else {
+              rb[li] = -1;
+              const unsigned long long slot = atomicAdd(&p.ctr->q_tail, 1ull);
+              StreamJob* jb = sp.jobs + slot;
+              jb->meta = ((unsigned long long)tile << 24) | ((unsigned long long)li << 12) |
+                         (unsigned long long)nheads;
+              st_release_u64(&jb->start_p1, (unsigned long long)(start + r) + 1ull);
+            }
+          }
+        }
+      }
+
+      // ---- output of tile T_{i-LAG}: coalesced stores of its short groups ----
+      if (!scan && out_tile >= 0) {
+        const int bo = (int)((i + 1) % NB);  // == (i - LAG) % NB
+        const int so = (s - LAG + STAGES) % STAGES;
+        named_bar(4 + bo, NSS);  // (D_{i-LAG}) wait for its base
+        const long long* s_key = stage0 + stage_words * so;
+        const int nheads = s_nheads[bo];
+        const long long base = (long long)s_base[bo];
+        const double* vb = s_val + (size_t)bo * TILE;
+        const short* rb = s_row + (size_t)bo * TILE;
+        unsigned int zeros = 0;
+        for (int li = tid; li < nheads; li += NSB) {
+          const int r = rb[li];
+          if (r < 0) continue;
+          const double v = vb[li];
+          p.out_vals[base + li] = v;
+          zeros += v == 0.0;
+          if constexpr (SRC == kSrcLinKey) {
+            long long lin = s_key[r];
+            long long* o = p.out_subs + (base + li) * p.out_nk;
+            for (int q = p.out_nk - 1; q >= 0; --q) {
+              const long long dm = p.dims[q];
+              o[q] = lin % dm;
+              lin /= dm;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c) {
+              if (NK == 0 && c >= nk) break;
+              p.out_subs[(base + li) * p.out_nk + c] = s_key[c * ROWS + r];
+            }
+          }
+        }
+        if (zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
+        named_bar(1, NSB);  // stage `so` consumed
+        if (tid == 0) acquire_issue(so);
+      }
+      s = (s + 1) % STAGES;
+    }
+    if (!scan) {
+      if (flags) atomicOr(&s_flags, flags);
+      named_bar(1, NSB);
+      if (tid == 0) {
+        if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+        __threadfence();
+        atomicAdd(&p.ctr->streamers_done, 1u);
+      }
+    }
+    return;
+  }
+
+  // ===================================== chain warps =====================================
+  double* cbuf = chain_buf + (size_t)(warp - kScanWarp - 1) * kChunk;
+  while (true) {
+    unsigned long long t = 0;
+    long long start = -1;
+    unsigned long long meta = 0;
+    if (lane == 0) {
+      t = atomicAdd(&p.ctr->q_head, 1ull);
+      while (true) {
+        if (t < ld_relaxed_u64(&p.ctr->q_tail)) {
+          unsigned long long sp1;
+          while ((sp1 = ld_relaxed_u64(&sp.jobs[t].start_p1)) == 0) __nanosleep(32);
+          start = (long long)(sp1 - 1);
+          meta = ld_relaxed_u64(&sp.jobs[t].meta);
+          sp.jobs[t].start_p1 = 0;  // self-cleaning queue
+          break;
+        }
+        if (ld_relaxed_u32(&p.ctr->streamers_done) == gridDim.x) {
+          if (t < ld_relaxed_u64(&p.ctr->q_tail)) continue;
+          break;
+        }
+        __nanosleep(256);
+      }
+    }
+    start = __shfl_sync(0xffffffffu, start, 0);
+    if (start < 0) break;
+    meta = __shfl_sync(0xffffffffu, meta, 0);
+    long long gk[NK > 0 ? NK : kMaxKeep];
+#pragma unroll
+    for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c)
+      if (NK > 0 || c < nk) gk[c] = __ldcg(p.key[c] + start);
+
+    double acc = 0.0;
+    bool first = true;
+    long long pos = start;
+    double av[8];
+    long long sk[8];
+    bool same[8];
+    auto load_chunk = [&](long long b0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const long long r = b0 + q * 32 + lane;
+        same[q] = r < p.n && key_eq_global<SRC, NK>(p, nk, r, gk);
+        av[q] = r < p.n ? __ldcg(p.a + r) : 0.0;
+        if constexpr (SRC == kSrcRaw) sk[q] = r < p.n ? __ldcg(p.subk + r) : 0;
+      }
+    };
+    load_chunk(pos);
+    while (true) {
+      int end = kChunk;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double w = av[q];
+        if constexpr (SRC == kSrcRaw) w = (sk[q] < 0 || sk[q] >= p.nx) ? 0.0 : __dmul_rn(w, __ldg(p.x + sk[q]));
+        cbuf[q * 32 + lane] = w;
+        const unsigned int mm = __ballot_sync(0xffffffffu, !same[q]);
+        if (mm && end == kChunk) end = q * 32 + __ffs(mm) - 1;
+      }
+      __syncwarp();
+      const bool more = end == kChunk;
+      if (more) load_chunk(pos + kChunk);  // in flight while lane 0 folds
+      if (lane == 0) {
+        int j = 0;
+        if (first) {
+          acc = cbuf[0];
+          j = 1;
+        }
+        acc = fold_run(cbuf, j, end, acc);
+      }
+      first = false;
+      __syncwarp();
+      if (!more) break;
+      pos += kChunk;
+    }
+    // output slot = tile base (its published inclusive prefix minus its aggregate) + local id
+    if (lane == 0) {
+      const long long tile = (long long)(meta >> 24);
+      const unsigned long long li = (meta >> 12) & 0xfff, agg = meta & 0xfff;
+      unsigned long long stw;
+      while (((stw = ld_relaxed(p.status + tile)) >> 62) != 2) __nanosleep(64);
+      const long long g = (long long)((stw & kStVal) - agg + li);
+      seg_emit<SRC>(p, g, gk, acc);
+    }
+  }
+}
+
+}  // namespace tk

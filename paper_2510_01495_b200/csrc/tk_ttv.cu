@@ -23,7 +23,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "tk_host.h"
-#include "tk_stream.cuh"
+#include "tk_stream_kernel.cuh"
 #include "tk_ttv_kernels.cuh"
 
 namespace tk {
@@ -397,14 +397,16 @@ int stream_jobs(long long cap, StreamJob** out) {
 
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  constexpr int TILE = NK > 0 ? 1024 : 512;
+  // geometry: 1 CTA per SM; LAG=2 tiles of slack for the look-back; 2-3 tiles in flight
+  constexpr int TILE = NK > 0 ? 1024 : 256;
   constexpr int HALO = 32;
-  constexpr int STAGES = 2;
-  constexpr int MINB = NK > 0 ? 2 : 1;
+  constexpr int LAG = 2;
+  constexpr int STAGES = (NK == 0) ? 4 : (NK + (SRC == kSrcRaw ? 2 : 1) <= 4 ? 5 : 4);
+  constexpr int LBD = 16;  // look-back window 512 tiles per round trip
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
-  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES>(ncol, nk);
-  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, MINB>;
+  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES, LAG>(ncol, nk);
+  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, LAG, LBD, 1>;
   set_smem_once(kern, smem);
   int per_sm = 0;
   TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));
