@@ -1,10 +1,12 @@
 // tk_stream_kernel.cuh -- the persistent streaming TTV kernel (see tk_stream.cuh for the roles).
 //
-// Software pipeline per CTA (iteration i handles tile T_i):
-//   streamers: [wait TMA T_i] head pass T_i | folds T_i | output T_{i-LAG} | refill its stage
-//   scan warp:                 popcount T_i, publish aggregate, look-back T_i  -> arrive D_i
-// The output of T_i waits on D_i only LAG iterations later, so the look-back latency (one or
-// more L2 round trips) is hidden behind LAG tiles of streaming work.
+// Software pipeline per CTA (iteration i handles tile T_i, ring slot b = i % NB):
+//   streamers: [wait TMA T_i] head pass | popcount prefix (registers) | hand (T_i, agg) to the
+//              scan warp (arrive FULL_b) | folds T_i | [sync DONE_{b'}] output T_{i-LAG} | refill
+//   scan warp: [sync FULL_b] look-back T_i -> base | arrive DONE_b          (fully asynchronous)
+// The output of T_i consumes its base LAG iterations later, so the look-back latency (one or
+// more L2 round trips) is hidden behind LAG tiles of streaming work, and nothing in the
+// streamer loop waits on the scan warp except that deferred output.
 #pragma once
 
 #include "tk_stream.cuh"
@@ -28,12 +30,13 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
   constexpr int TWORDS = TILE / 32;
   constexpr int ITER = (ROWS + 255) / 256;
   constexpr int OWN = TILE / 256;  // rows owned per streamer thread (blocked)
-  constexpr int NB = LAG + 1;      // fold-result buffers / look-back barriers in flight
+  constexpr int NB = LAG + 1;      // ring slots: fold results, look-back hand-off
   constexpr int NSB = kStreamWarps * 32;
   constexpr int NSS = NSB + 32;    // streamers + scan warp
-  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE < 4096, "tile geometry");
+  constexpr int kFull = 2, kDone = 2 + NB;  // named barrier ids (1 = streamers only)
+  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE < 4096 && TWORDS <= 32, "tile geometry");
   static_assert(STAGES >= LAG + 2, "a stage per pending tile plus one in flight");
-  static_assert(4 + NB <= 16, "named barrier ids");
+  static_assert(kDone + NB <= 16, "named barrier ids");
   const SegParams& p = sp.s;
   const int nk = seg_nk<SRC, NK>(p);
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
@@ -48,7 +51,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
   __shared__ long long s_stage_tile[STAGES];
   __shared__ int s_stage_bulk[STAGES];
   __shared__ unsigned int s_head[WORDS];
-  __shared__ int s_wpref[TWORDS];
+  __shared__ long long s_lb_tile[NB];
   __shared__ int s_nheads[NB];
   __shared__ unsigned long long s_base[NB];
   __shared__ unsigned int s_flags;
@@ -60,9 +63,29 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
   }
   __syncthreads();
 
-  if (warp <= kScanWarp) {
-    const bool scan = warp == kScanWarp;
-    auto acquire_issue = [&](int s) {  // streamer thread 0 only
+  if (warp == kScanWarp) {
+    // ========================= scan warp: asynchronous look-backs =========================
+    for (long long k = 0;; ++k) {
+      const int b = (int)(k % NB);
+      named_bar(kFull + b, NSS);
+      const long long tile = s_lb_tile[b];
+      if (tile < 0) break;
+      const unsigned long long agg = (unsigned long long)s_nheads[b];
+      const unsigned long long excl = lookback_wide<LBD>(p.status, tile, agg);
+      if (lane == 0) {
+        s_base[b] = excl;
+        const long long start = tile * TILE;
+        if (start + min((long long)TILE, p.n - start) == p.n) p.ctr->groups = excl + agg;
+      }
+      __syncwarp();
+      named_arrive(kDone + b, NSS);
+    }
+    return;
+  }
+
+  if (warp < kStreamWarps) {
+    // ==================================== streamers ====================================
+    auto acquire_issue = [&](int s) {  // thread 0 only
       const unsigned int t = atomicAdd(&p.ctr->tile_ticket, 1u);
       if ((long long)t >= sp.ntiles) {
         s_stage_tile[s] = -1;
@@ -111,8 +134,9 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
 #pragma unroll
     for (int k = 0; k < LAG; ++k) hist[k] = -1;
     int s = 0;
-    for (long long i = 0;; ++i) {
-      named_bar(2, NSS);  // (A) stage s descriptor visible
+    long long i = 0;
+    for (;; ++i) {
+      named_bar(1, NSB);  // (A) stage s descriptor visible; previous tile's smem reads done
       const long long tile = s_stage_tile[s];
       const long long out_tile = hist[LAG - 1];  // tile of iteration i - LAG
       bool any = tile >= 0 || out_tile >= 0;
@@ -134,136 +158,113 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
         const long long start = tile * TILE;
         const int cnt = (int)min((long long)TILE, p.n - start);
         const int avail = (int)min((long long)ROWS, p.n - start);
-        if (!scan) {
-          if (s_stage_bulk[s]) {
-            mbar_wait(&s_full[s], (phase >> s) & 1u);
-            phase ^= 1u << s;
-          } else {
-            for (int r = tid; r < avail; r += NSB) {
-              for (int c = 0; c < nk; ++c) s_key[c * ROWS + r] = p.key[c][start + r];
-              s_a[r] = p.a[start + r];
-              if constexpr (SRC == kSrcRaw) st[(size_t)(nk + 1) * ROWS + r] = p.subk[start + r];
-            }
-            if (tid < nk && start > 0) st[(size_t)ncol * ROWS + 2 * tid + 1] = p.key[tid][start - 1];
-            named_bar(1, NSB);
-          }
-          // ---- w and head flags (striped rows: conflict-free shared memory) ----
-#pragma unroll
-          for (int j = 0; j < ITER; ++j) {
-            const int r = j * 256 + tid;
-            bool head = false;
-            if (r < avail) {
-              if constexpr (SRC == kSrcRaw) {
-                const long long idx = s_subk[r];
-                double w = 0.0;
-                if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
-                else w = __dmul_rn(s_a[r], __ldg(p.x + idx));
-                s_a[r] = w;
-              }
-              int cmp = 0;
-#pragma unroll
-              for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c) {
-                if (NK == 0 && c >= nk) break;
-                const long long va = s_key[c * ROWS + r];
-                const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
-                if (va != vb) {
-                  cmp = va < vb ? -1 : 1;
-                  break;
-                }
-              }
-              if (r == 0 && start == 0) cmp = 1;
-              head = cmp != 0;
-              if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
-            }
-            const unsigned int m = __ballot_sync(0xffffffffu, head);
-            const int wi = j * 8 + warp;
-            if (lane == 0 && wi < WORDS) s_head[wi] = m;
-          }
-        }
-        named_bar(2, NSS);  // (B) heads ready
-
-        if (scan) {
-          constexpr int PL = (TWORDS + 31) / 32;
-          int cw[PL];
-          int mine = 0;
-#pragma unroll
-          for (int q = 0; q < PL; ++q) {
-            const int wi = lane * PL + q;
-            unsigned int word = 0;
-            if (wi < TWORDS && wi * 32 < cnt) {
-              word = s_head[wi];
-              if (wi * 32 + 32 > cnt) word &= (1u << (cnt - wi * 32)) - 1u;
-            }
-            cw[q] = __popc(word);
-            mine += cw[q];
-          }
-          int incl = mine;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-          }
-          int run = incl - mine;
-#pragma unroll
-          for (int q = 0; q < PL; ++q) {
-            const int wi = lane * PL + q;
-            if (wi < TWORDS) s_wpref[wi] = run;
-            run += cw[q];
-          }
-          const int agg = __shfl_sync(0xffffffffu, incl, 31);
-          if (lane == 0) s_nheads[b] = agg;
-          lookback_publish_agg<LBD>(p.status, tile, (unsigned long long)agg);
-          __syncwarp();
-          named_bar(3, NSS);  // (C) local ids ready
-          const unsigned long long excl = lookback_wide<LBD>(p.status, tile, (unsigned long long)agg);
-          if (lane == 0) {
-            s_base[b] = excl;
-            if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
-          }
-          __syncwarp();
-          named_arrive(4 + b, NSS);  // (D_i) base of tile i ready
+        if (s_stage_bulk[s]) {
+          mbar_wait(&s_full[s], (phase >> s) & 1u);
+          phase ^= 1u << s;
         } else {
-          named_bar(3, NSS);  // (C)
-          const int nheads = s_nheads[b];
-          double* vb = s_val + (size_t)b * TILE;
-          short* rb = s_row + (size_t)b * TILE;
-          const int r0 = tid * OWN;
+          for (int r = tid; r < avail; r += NSB) {
+            for (int c = 0; c < nk; ++c) s_key[c * ROWS + r] = p.key[c][start + r];
+            s_a[r] = p.a[start + r];
+            if constexpr (SRC == kSrcRaw) st[(size_t)(nk + 1) * ROWS + r] = p.subk[start + r];
+          }
+          if (tid < nk && start > 0) st[(size_t)ncol * ROWS + 2 * tid + 1] = p.key[tid][start - 1];
+          named_bar(1, NSB);
+        }
+        // ---- w and head flags (striped rows: conflict-free shared memory) ----
+#pragma unroll
+        for (int j = 0; j < ITER; ++j) {
+          const int r = j * 256 + tid;
+          bool head = false;
+          if (r < avail) {
+            if constexpr (SRC == kSrcRaw) {
+              const long long idx = s_subk[r];
+              double w = 0.0;
+              if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+              else w = __dmul_rn(s_a[r], __ldg(p.x + idx));
+              s_a[r] = w;
+            }
+            int cmp = 0;
+#pragma unroll
+            for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c) {
+              if (NK == 0 && c >= nk) break;
+              const long long va = s_key[c * ROWS + r];
+              const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
+              if (va != vb) {
+                cmp = va < vb ? -1 : 1;
+                break;
+              }
+            }
+            if (r == 0 && start == 0) cmp = 1;
+            head = cmp != 0;
+            if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
+          }
+          const unsigned int m = __ballot_sync(0xffffffffu, head);
+          const int wi = j * 8 + warp;
+          if (lane == 0 && wi < WORDS) s_head[wi] = m;
+        }
+        named_bar(1, NSB);  // (B) heads visible to all streamer warps
+
+        // ---- popcount prefix over the tile's words, one word per lane, in every warp ----
+        unsigned int myword = 0;
+        if (lane < TWORDS && lane * 32 < cnt) {
+          myword = s_head[lane];
+          if (lane * 32 + 32 > cnt) myword &= (1u << (cnt - lane * 32)) - 1u;
+        }
+        int incl = __popc(myword);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int wpref = incl - __popc(myword);  // exclusive prefix of word `lane`
+        const int agg = __shfl_sync(0xffffffffu, incl, 31);
+        if (tid == 0) {
+          lookback_publish_agg<LBD>(p.status, tile, (unsigned long long)agg);
+          s_lb_tile[b] = tile;
+          s_nheads[b] = agg;
+        }
+        named_arrive(kFull + b, NSS);  // hand (tile, agg) to the scan warp
+
+        // ---- folds (blocked row ownership); long / spanning groups -> chain jobs ----
+        double* vb = s_val + (size_t)b * TILE;
+        short* rb = s_row + (size_t)b * TILE;
+        const int r0 = tid * OWN;
+        // the OWN rows of this thread lie in word r0 >> 5
+        const int wp_own = __shfl_sync(0xffffffffu, wpref, (r0 >> 5) & 31);
 #pragma unroll 1
-          for (int q = 0; q < OWN; ++q) {
-            const int r = r0 + q;
-            if (r >= cnt) break;
-            const unsigned int word = s_head[r >> 5];
-            if (!((word >> (r & 31)) & 1u)) continue;
-            const int li = s_wpref[r >> 5] + __popc(word & ((1u << (r & 31)) - 1u));
-            int end = avail;
-            {
-              const int q1 = r + 1;
-              int wi = q1 >> 5;
-              unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
-              while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
-              if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
-            }
-            const bool open = end == avail && start + avail < p.n;
-            if (!open && end - r <= kShort) {
-              vb[li] = fold_run(s_a, r + 1, end, s_a[r]);
-              rb[li] = (short)r;
-            } else {
-              rb[li] = -1;
-              const unsigned long long slot = atomicAdd(&p.ctr->q_tail, 1ull);
-              StreamJob* jb = sp.jobs + slot;
-              jb->meta = ((unsigned long long)tile << 24) | ((unsigned long long)li << 12) |
-                         (unsigned long long)nheads;
-              st_release_u64(&jb->start_p1, (unsigned long long)(start + r) + 1ull);
-            }
+        for (int q = 0; q < OWN; ++q) {
+          const int r = r0 + q;
+          if (r >= cnt) break;
+          const unsigned int word = s_head[r >> 5];
+          if (!((word >> (r & 31)) & 1u)) continue;
+          const int li = wp_own + __popc(word & ((1u << (r & 31)) - 1u));
+          int end = avail;
+          {
+            const int q1 = r + 1;
+            int wi = q1 >> 5;
+            unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
+            while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
+            if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
+          }
+          const bool open = end == avail && start + avail < p.n;
+          if (!open && end - r <= kShort) {
+            vb[li] = fold_run(s_a, r + 1, end, s_a[r]);
+            rb[li] = (short)r;
+          } else {
+            rb[li] = -1;
+            const unsigned long long slot = atomicAdd(&p.ctr->q_tail, 1ull);
+            StreamJob* jb = sp.jobs + slot;
+            jb->meta = ((unsigned long long)tile << 24) | ((unsigned long long)li << 12) | (unsigned long long)agg;
+            st_release_u64(&jb->start_p1, (unsigned long long)(start + r) + 1ull);
           }
         }
       }
 
       // ---- output of tile T_{i-LAG}: coalesced stores of its short groups ----
-      if (!scan && out_tile >= 0) {
+      if (out_tile >= 0) {
         const int bo = (int)((i + 1) % NB);  // == (i - LAG) % NB
         const int so = (s - LAG + STAGES) % STAGES;
-        named_bar(4 + bo, NSS);  // (D_{i-LAG}) wait for its base
+        named_bar(kDone + bo, NSS);  // wait for its base
         const long long* s_key = stage0 + stage_words * so;
         const int nheads = s_nheads[bo];
         const long long base = (long long)s_base[bo];
@@ -298,14 +299,18 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
       }
       s = (s + 1) % STAGES;
     }
-    if (!scan) {
-      if (flags) atomicOr(&s_flags, flags);
-      named_bar(1, NSB);
-      if (tid == 0) {
-        if (s_flags) atomicOr(&p.ctr->flags, s_flags);
-        __threadfence();
-        atomicAdd(&p.ctr->streamers_done, 1u);
-      }
+    // stop the scan warp: sentinel in the next ring slot (every earlier slot is drained).
+    // Tiles were processed in iterations 0..ntile-1 (tickets are monotonic), so the slot
+    // the scan warp waits on is ntile % NB.
+    const long long ntile = i - LAG < 0 ? 0 : i - LAG;
+    if (tid == 0) s_lb_tile[(int)(ntile % NB)] = -1;
+    named_arrive(kFull + (int)(ntile % NB), NSS);
+    if (flags) atomicOr(&s_flags, flags);
+    named_bar(1, NSB);
+    if (tid == 0) {
+      if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+      __threadfence();
+      atomicAdd(&p.ctr->streamers_done, 1u);
     }
     return;
   }
@@ -331,7 +336,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
           if (t < ld_relaxed_u64(&p.ctr->q_tail)) continue;
           break;
         }
-        __nanosleep(256);
+        __nanosleep(512);
       }
     }
     start = __shfl_sync(0xffffffffu, start, 0);
