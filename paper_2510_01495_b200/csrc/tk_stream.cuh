@@ -36,6 +36,20 @@ struct StreamParams {
   SegParams s;          // stream description + outputs + status/ctr
   StreamJob* jobs;      // self-cleaning: all-zero on entry and on exit
   long long ntiles;
+  unsigned long long* prof;  // optional per-CTA cycle counters [grid][16] (TK_STREAM_PROFILE=1)
+};
+
+// Optional phase timing (development instrumentation; off unless prof != nullptr).
+#define TKP_START(var) const long long var = (sp.prof ? clock64() : 0)
+#define TKP_ADD(slot, var)                                                                        \
+  do {                                                                                            \
+    if (sp.prof) atomicAdd(sp.prof + blockIdx.x * 16 + (slot), (unsigned long long)(clock64() - (var))); \
+  } while (0)
+#define TKP_COUNT(slot, v)                                                        \
+  do {                                                                            \
+    if (sp.prof) atomicAdd(sp.prof + blockIdx.x * 16 + (slot), (unsigned long long)(v)); \
+  } while (0)
+struct StreamProfDummy_ {
 };
 
 constexpr int kStreamWarps = 8;

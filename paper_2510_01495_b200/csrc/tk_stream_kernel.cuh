@@ -67,11 +67,15 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
     // ========================= scan warp: asynchronous look-backs =========================
     for (long long k = 0;; ++k) {
       const int b = (int)(k % NB);
+      TKP_START(t_w);
       named_bar(kFull + b, NSS);
+      if (lane == 0) TKP_ADD(8, t_w);
       const long long tile = s_lb_tile[b];
       if (tile < 0) break;
       const unsigned long long agg = (unsigned long long)s_nheads[b];
+      TKP_START(t_l);
       const unsigned long long excl = lookback_wide<LBD>(p.status, tile, agg);
+      if (lane == 0) TKP_ADD(9, t_l);
       if (lane == 0) {
         s_base[b] = excl;
         const long long start = tile * TILE;
@@ -85,8 +89,13 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
 
   if (warp < kStreamWarps) {
     // ==================================== streamers ====================================
+    // Static round-robin tiles (CTA c: c, c+G, c+2G, ...): every CTA processes its k-th tile
+    // in the same wave as its neighbours, so a look-back finds its predecessors' aggregates
+    // published by CTAs working in lock-step, not by one that prefetched far ahead.
+    long long next_tile = blockIdx.x;
     auto acquire_issue = [&](int s) {  // thread 0 only
-      const unsigned int t = atomicAdd(&p.ctr->tile_ticket, 1u);
+      const long long t = next_tile;
+      next_tile += gridDim.x;
       if ((long long)t >= sp.ntiles) {
         s_stage_tile[s] = -1;
         return;
@@ -136,7 +145,9 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
     int s = 0;
     long long i = 0;
     for (;; ++i) {
+      TKP_START(t_a);
       named_bar(1, NSB);  // (A) stage s descriptor visible; previous tile's smem reads done
+      if (tid == 0) TKP_ADD(6, t_a);
       const long long tile = s_stage_tile[s];
       const long long out_tile = hist[LAG - 1];  // tile of iteration i - LAG
       bool any = tile >= 0 || out_tile >= 0;
@@ -158,9 +169,11 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
         const long long start = tile * TILE;
         const int cnt = (int)min((long long)TILE, p.n - start);
         const int avail = (int)min((long long)ROWS, p.n - start);
+        TKP_START(t_m);
         if (s_stage_bulk[s]) {
           mbar_wait(&s_full[s], (phase >> s) & 1u);
           phase ^= 1u << s;
+          if (tid == 0) TKP_ADD(0, t_m);
         } else {
           for (int r = tid; r < avail; r += NSB) {
             for (int c = 0; c < nk; ++c) s_key[c * ROWS + r] = p.key[c][start + r];
@@ -202,7 +215,11 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
           const int wi = j * 8 + warp;
           if (lane == 0 && wi < WORDS) s_head[wi] = m;
         }
+        if (tid == 0) TKP_ADD(1, t_m);
+        TKP_START(t_b);
         named_bar(1, NSB);  // (B) heads visible to all streamer warps
+        if (tid == 0) TKP_ADD(2, t_b);
+        TKP_START(t_f);
 
         // ---- popcount prefix over the tile's words, one word per lane, in every warp ----
         unsigned int myword = 0;
@@ -258,13 +275,17 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
             st_release_u64(&jb->start_p1, (unsigned long long)(start + r) + 1ull);
           }
         }
+        if (tid == 0) TKP_ADD(3, t_f);
       }
 
       // ---- output of tile T_{i-LAG}: coalesced stores of its short groups ----
       if (out_tile >= 0) {
         const int bo = (int)((i + 1) % NB);  // == (i - LAG) % NB
         const int so = (s - LAG + STAGES) % STAGES;
+        TKP_START(t_d);
         named_bar(kDone + bo, NSS);  // wait for its base
+        if (tid == 0) TKP_ADD(4, t_d);
+        TKP_START(t_o);
         const long long* s_key = stage0 + stage_words * so;
         const int nheads = s_nheads[bo];
         const long long base = (long long)s_base[bo];
@@ -296,6 +317,8 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
         if (zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
         named_bar(1, NSB);  // stage `so` consumed
         if (tid == 0) acquire_issue(so);
+        if (tid == 0) TKP_ADD(5, t_o);
+        if (tid == 0) TKP_COUNT(7, 1);
       }
       s = (s + 1) % STAGES;
     }
@@ -321,6 +344,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
     unsigned long long t = 0;
     long long start = -1;
     unsigned long long meta = 0;
+    TKP_START(t_idle);
     if (lane == 0) {
       t = atomicAdd(&p.ctr->q_head, 1ull);
       while (true) {
@@ -340,7 +364,9 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
       }
     }
     start = __shfl_sync(0xffffffffu, start, 0);
+    if (lane == 0) TKP_ADD(10, t_idle);
     if (start < 0) break;
+    TKP_START(t_busy);
     meta = __shfl_sync(0xffffffffu, meta, 0);
     long long gk[NK > 0 ? NK : kMaxKeep];
 #pragma unroll
@@ -397,6 +423,9 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
       while (((stw = ld_relaxed(p.status + tile)) >> 62) != 2) __nanosleep(64);
       const long long g = (long long)((stw & kStVal) - agg + li);
       seg_emit<SRC>(p, g, gk, acc);
+      TKP_ADD(11, t_busy);
+      TKP_COUNT(12, 1);
+      TKP_COUNT(13, pos - start + kChunk);
     }
   }
 }

@@ -429,6 +429,13 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   sp.ntiles = ntiles;
   TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
   const unsigned grid = (unsigned)(per_sm * num_sms());
+  DevBuf prof;
+  const bool profile = getenv("TK_STREAM_PROFILE") != nullptr;
+  if (profile) {
+    if (int rc = prof.alloc((size_t)grid * 16 * 8, st)) return rc;
+    TK_CUDA(cudaMemsetAsync(prof.get(), 0, (size_t)grid * 16 * 8, st));
+    sp.prof = prof.as<unsigned long long>();
+  }
   void* args[] = {&sp};
   ktimer_begin(st);
   TK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kStreamThreads), args, smem, st));
@@ -436,6 +443,22 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   count_launch();
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
+  if (profile) {
+    std::vector<unsigned long long> h((size_t)grid * 16);
+    TK_CUDA(cudaMemcpy(h.data(), prof.get(), h.size() * 8, cudaMemcpyDeviceToHost));
+    static const char* names[16] = {"tma_wait", "head(+wait)", "bar_B", "folds", "wait_base", "output",
+                                    "bar_A", "tiles", "scan_idle", "scan_lookback", "chain_idle", "chain_busy",
+                                    "chain_jobs", "chain_rows", "", ""};
+    fprintf(stderr, "[tk stream profile] grid=%u ntiles=%lld (per-CTA mean; cycles->us at 1.965 GHz)\n", grid,
+            ntiles);
+    for (int k = 0; k < 14; ++k) {
+      double sum = 0;
+      for (unsigned c = 0; c < grid; ++c) sum += (double)h[(size_t)c * 16 + k];
+      const double mean = sum / grid;
+      if (k == 7 || k == 12 || k == 13) fprintf(stderr, "  %-14s %14.1f (total %.0f)\n", names[k], mean, sum);
+      else fprintf(stderr, "  %-14s %14.1f us\n", names[k], mean / 1965.0);
+    }
+  }
   return TK_OK;
 }
 
