@@ -25,12 +25,13 @@
 
 namespace tk {
 
-// job record: start row + 1 (0 = empty slot; written last, with release semantics) and
-// (tile, local group index, tile head count) packed into one word.
-struct StreamJob {
-  unsigned long long start_p1;
-  unsigned long long meta;  // tile << 24 | local << 12 | agg   (TILE <= 4096)
-};
+// A chain job is ONE 64-bit word (so publishing it needs no fence):
+//   [63:21] first row + 1 (never 0: 0 marks an empty slot)  [20:11] local group id  [10:0] tile head count
+// The tile is first_row / TILE; the output slot is base(tile) + local id.
+__host__ __device__ __forceinline__ unsigned long long job_pack(long long row, int li, int agg) {
+  return ((unsigned long long)(row + 1) << 21) | ((unsigned long long)li << 11) | (unsigned long long)agg;
+}
+typedef unsigned long long StreamJob;
 
 struct StreamParams {
   SegParams s;          // stream description + outputs + status/ctr
@@ -54,7 +55,7 @@ struct StreamProfDummy_ {
 
 constexpr int kStreamWarps = 8;
 constexpr int kScanWarp = 8;
-constexpr int kChainWarps = 4;
+constexpr int kChainWarps = 8;
 constexpr int kStreamThreads = (kStreamWarps + 1 + kChainWarps) * 32;
 constexpr int kShort = 64;   // in-thread fold limit (rows)
 constexpr int kChunk = 256;  // chain-warp chunk (8 rows per lane)

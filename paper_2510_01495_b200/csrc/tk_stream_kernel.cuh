@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
   constexpr int NSB = kStreamWarps * 32;
   constexpr int NSS = NSB + 32;    // streamers + scan warp
   constexpr int kFull = 2, kDone = 2 + NB;  // named barrier ids (1 = streamers only)
-  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE < 4096 && TWORDS <= 32, "tile geometry");
+  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE <= 1024 && TWORDS <= 32, "tile geometry (job packing: 10-bit local id)");
   static_assert(STAGES >= LAG + 2, "a stage per pending tile plus one in flight");
   static_assert(kDone + NB <= 16, "named barrier ids");
   const SegParams& p = sp.s;
@@ -184,18 +184,33 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
           named_bar(1, NSB);
         }
         // ---- w and head flags (striped rows: conflict-free shared memory) ----
+        if constexpr (SRC == kSrcRaw) {
+          // all gathers in flight before any store: a store to s_a could alias the
+          // later loads for the compiler, which would serialise ITER L2 round trips
+          double xv[ITER], av[ITER];
+#pragma unroll
+          for (int j = 0; j < ITER; ++j) {
+            const int r = j * 256 + tid;
+            xv[j] = 0.0;
+            av[j] = 0.0;
+            if (r < avail) {
+              const long long idx = s_subk[r];
+              av[j] = s_a[r];
+              if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+              else xv[j] = __ldg(p.x + idx);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < ITER; ++j) {
+            const int r = j * 256 + tid;
+            if (r < avail) s_a[r] = __dmul_rn(av[j], xv[j]);
+          }
+        }
 #pragma unroll
         for (int j = 0; j < ITER; ++j) {
           const int r = j * 256 + tid;
           bool head = false;
           if (r < avail) {
-            if constexpr (SRC == kSrcRaw) {
-              const long long idx = s_subk[r];
-              double w = 0.0;
-              if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
-              else w = __dmul_rn(s_a[r], __ldg(p.x + idx));
-              s_a[r] = w;
-            }
             int cmp = 0;
 #pragma unroll
             for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c) {
@@ -269,10 +284,9 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
             rb[li] = (short)r;
           } else {
             rb[li] = -1;
+            // one 64-bit word = the whole job: no fence needed to publish it
             const unsigned long long slot = atomicAdd(&p.ctr->q_tail, 1ull);
-            StreamJob* jb = sp.jobs + slot;
-            jb->meta = ((unsigned long long)tile << 24) | ((unsigned long long)li << 12) | (unsigned long long)agg;
-            st_release_u64(&jb->start_p1, (unsigned long long)(start + r) + 1ull);
+            st_relaxed(sp.jobs + slot, job_pack(start + r, li, agg));
           }
         }
         if (tid == 0) TKP_ADD(3, t_f);
@@ -339,21 +353,22 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
   }
 
   // ===================================== chain warps =====================================
+  // Each warp drains jobs: a job is a group that is long or crosses its tile.  Rows stream in
+  // 256-row chunks (8 per lane, coalesced, L2-hot); the x gathers of a chunk are issued
+  // together; lane 0 folds the chunk serially from smem while the next chunk is in flight.
   double* cbuf = chain_buf + (size_t)(warp - kScanWarp - 1) * kChunk;
+  constexpr int NKR = NK > 0 ? NK : kMaxKeep;
   while (true) {
-    unsigned long long t = 0;
     long long start = -1;
-    unsigned long long meta = 0;
+    unsigned long long job = 0;
     TKP_START(t_idle);
     if (lane == 0) {
-      t = atomicAdd(&p.ctr->q_head, 1ull);
+      const unsigned long long t = atomicAdd(&p.ctr->q_head, 1ull);
       while (true) {
         if (t < ld_relaxed_u64(&p.ctr->q_tail)) {
-          unsigned long long sp1;
-          while ((sp1 = ld_relaxed_u64(&sp.jobs[t].start_p1)) == 0) __nanosleep(32);
-          start = (long long)(sp1 - 1);
-          meta = ld_relaxed_u64(&sp.jobs[t].meta);
-          sp.jobs[t].start_p1 = 0;  // self-cleaning queue
+          while ((job = ld_relaxed_u64(sp.jobs + t)) == 0) __nanosleep(32);
+          sp.jobs[t] = 0;  // self-cleaning queue
+          start = (long long)(job >> 21) - 1;
           break;
         }
         if (ld_relaxed_u32(&p.ctr->streamers_done) == gridDim.x) {
@@ -367,36 +382,45 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
     if (lane == 0) TKP_ADD(10, t_idle);
     if (start < 0) break;
     TKP_START(t_busy);
-    meta = __shfl_sync(0xffffffffu, meta, 0);
-    long long gk[NK > 0 ? NK : kMaxKeep];
-#pragma unroll
-    for (int c = 0; c < (NK > 0 ? NK : kMaxKeep); ++c)
-      if (NK > 0 || c < nk) gk[c] = __ldcg(p.key[c] + start);
+    job = __shfl_sync(0xffffffffu, job, 0);
 
+    long long gk[NKR];
     double acc = 0.0;
     bool first = true;
     long long pos = start;
+    long long kv[8][NKR];
     double av[8];
     long long sk[8];
-    bool same[8];
     auto load_chunk = [&](long long b0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const long long r = b0 + q * 32 + lane;
-        same[q] = r < p.n && key_eq_global<SRC, NK>(p, nk, r, gk);
-        av[q] = r < p.n ? __ldcg(p.a + r) : 0.0;
-        if constexpr (SRC == kSrcRaw) sk[q] = r < p.n ? __ldcg(p.subk + r) : 0;
+        const bool ok = r < p.n;
+#pragma unroll
+        for (int c = 0; c < NKR; ++c)
+          if (NK > 0 || c < nk) kv[q][c] = ok ? __ldcg(p.key[c] + r) : 0;
+        av[q] = ok ? __ldcg(p.a + r) : 0.0;
+        if constexpr (SRC == kSrcRaw) sk[q] = ok ? __ldcg(p.subk + r) : 0;
       }
     };
     load_chunk(pos);
+#pragma unroll
+    for (int c = 0; c < NKR; ++c) gk[c] = __shfl_sync(0xffffffffu, kv[0][c], 0);  // the group's key
     while (true) {
+      double xv[8];
+      if constexpr (SRC == kSrcRaw) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xv[q] = (sk[q] < 0 || sk[q] >= p.nx) ? 0.0 : __ldg(p.x + sk[q]);
+      }
       int end = kChunk;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        double w = av[q];
-        if constexpr (SRC == kSrcRaw) w = (sk[q] < 0 || sk[q] >= p.nx) ? 0.0 : __dmul_rn(w, __ldg(p.x + sk[q]));
-        cbuf[q * 32 + lane] = w;
-        const unsigned int mm = __ballot_sync(0xffffffffu, !same[q]);
+        bool same = pos + q * 32 + lane < p.n;
+#pragma unroll
+        for (int c = 0; c < NKR; ++c)
+          if (NK > 0 || c < nk) same = same && kv[q][c] == gk[c];
+        cbuf[q * 32 + lane] = (SRC == kSrcRaw) ? __dmul_rn(av[q], xv[q]) : av[q];
+        const unsigned int mm = __ballot_sync(0xffffffffu, !same);
         if (mm && end == kChunk) end = q * 32 + __ffs(mm) - 1;
       }
       __syncwarp();
@@ -412,20 +436,22 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) ttv_stream_kernel(Stream
       }
       first = false;
       __syncwarp();
-      if (!more) break;
+      if (!more) {
+        if (lane == 0) TKP_COUNT(13, pos - start + end);
+        break;
+      }
       pos += kChunk;
     }
     // output slot = tile base (its published inclusive prefix minus its aggregate) + local id
     if (lane == 0) {
-      const long long tile = (long long)(meta >> 24);
-      const unsigned long long li = (meta >> 12) & 0xfff, agg = meta & 0xfff;
+      const long long tile = start / TILE;
+      const unsigned long long li = (job >> 11) & 0x3ff, agg = job & 0x7ff;
       unsigned long long stw;
       while (((stw = ld_relaxed(p.status + tile)) >> 62) != 2) __nanosleep(64);
       const long long g = (long long)((stw & kStVal) - agg + li);
       seg_emit<SRC>(p, g, gk, acc);
       TKP_ADD(11, t_busy);
       TKP_COUNT(12, 1);
-      TKP_COUNT(13, pos - start + kChunk);
     }
   }
 }
