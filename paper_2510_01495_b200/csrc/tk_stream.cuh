@@ -35,7 +35,8 @@ typedef unsigned long long StreamJob;
 
 struct StreamParams {
   SegParams s;          // stream description + outputs + status/ctr
-  StreamJob* jobs;      // self-cleaning: all-zero on entry and on exit
+  StreamJob* jobs;      // [ntiles][kJobsPerTile] chain jobs: (row in tile << 16) | local id
+  unsigned long long* jcount;  // [ntiles] (base << 8) | (njobs + 1), 0 = not yet published
   long long ntiles;
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][16] (TK_STREAM_PROFILE=1)
 };

@@ -372,62 +372,37 @@ int grid_for(long long n, int per_thread = 4) {
   return (int)std::max(1LL, std::min(want, cap));
 }
 
-// Persistent, self-cleaning job queue per device (all-zero between calls: every pushed job
-// is consumed exactly once and its slot cleared by the consumer).  Grow-only.
-int stream_jobs(long long cap, StreamJob** out) {
-  static std::mutex mu;
-  static StreamJob* buf[64] = {};
-  static long long have[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  dev &= 63;
-  std::lock_guard<std::mutex> lk(mu);
-  if (cap > have[dev]) {
-    if (buf[dev]) TK_CUDA(cudaFree(buf[dev]));
-    buf[dev] = nullptr;
-    have[dev] = 0;
-    const long long want = std::max(cap, have[dev] * 2);
-    TK_CUDA(cudaMalloc(&buf[dev], (size_t)want * sizeof(StreamJob)));
-    TK_CUDA(cudaMemset(buf[dev], 0, (size_t)want * sizeof(StreamJob)));
-    have[dev] = want;
-  }
-  *out = buf[dev];
-  return TK_OK;
-}
-
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  // geometry: 1 CTA per SM; LAG=2 tiles of slack for the look-back; 2-3 tiles in flight
+  // geometry: 1 CTA per SM, a 3-slot TMA ring (~120 KB smem: L1 keeps x resident)
   constexpr int TILE = NK > 0 ? 1024 : 256;
   constexpr int HALO = 32;
-  constexpr int LAG = 2;
-  constexpr int STAGES = (NK == 0) ? 4 : (NK + (SRC == kSrcRaw ? 2 : 1) <= 4 ? 5 : 4);
-  constexpr int LBD = 16;  // look-back window 512 tiles per round trip
+  constexpr int STAGES = 3;
+  constexpr int LBD = 16;  // look-back window: 512 tiles per L2 round trip
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
-  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES, LAG>(ncol, nk);
-  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, LAG, LBD, 1>;
+  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES>(ncol, nk);
+  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, LBD>;
   set_smem_once(kern, smem);
   int per_sm = 0;
-  TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamThreads, smem));
+  TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsV6, smem));
   if (per_sm < 1) return fail(TK_EARG, "ttv: stream kernel does not fit on an SM");
+  per_sm = 1;
   const long long ntiles = (p.n + TILE - 1) / TILE;
-  // at most one open group per tile plus TILE/(kShort+1) long closed groups per tile
-  const long long job_cap = ntiles * (1 + TILE / (kShort + 1)) + 1;
-  StreamJob* jobs = nullptr;
-  if (int rc = stream_jobs(job_cap, &jobs)) return rc;
-  // scratch: look-back status | counters (zeroed per call)
+  // scratch: look-back status | counters | job counts (zeroed per call) | job slots
   const size_t status_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
+  const size_t jc_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
   DevBuf scratch;
-  if (int rc = scratch.alloc(status_b + 256, st)) return rc;
+  if (int rc = scratch.alloc(status_b + 256 + jc_b + (size_t)ntiles * kJobsPerTile * 8, st)) return rc;
   char* b = scratch.as<char>();
   p.status = reinterpret_cast<unsigned long long*>(b);
   p.ctr = reinterpret_cast<Counters*>(b + status_b);
   StreamParams sp{};
   sp.s = p;
-  sp.jobs = jobs;
+  sp.jcount = reinterpret_cast<unsigned long long*>(b + status_b + 256);
+  sp.jobs = reinterpret_cast<StreamJob*>(b + status_b + 256 + jc_b);
   sp.ntiles = ntiles;
-  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
+  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256 + jc_b, st));
   const unsigned grid = (unsigned)(per_sm * num_sms());
   DevBuf prof;
   const bool profile = getenv("TK_STREAM_PROFILE") != nullptr;
@@ -438,7 +413,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   }
   void* args[] = {&sp};
   ktimer_begin(st);
-  TK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kStreamThreads), args, smem, st));
+  TK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreadsV6), args, smem, st));
   ktimer_end(st);
   count_launch();
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
