@@ -25,7 +25,7 @@
 
 namespace tk {
 
-constexpr int kLookWarps = 4;
+constexpr int kLookWarps = 3;  // 20 warps total: 5 per SMSP x 96 registers = one SMSP register file
 constexpr int kJobsPerTile = 16;  // 1 open group + TILE/(kShort+1) long closed groups (TILE <= 1024)
 constexpr int kWarpsTotal = 1 + kLookWarps + kStreamWarps + kChainWarps;
 constexpr int kThreadsV6 = kWarpsTotal * 32;
