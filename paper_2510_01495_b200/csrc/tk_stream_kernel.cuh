@@ -1,38 +1,49 @@
 // tk_stream_kernel.cuh -- the persistent streaming TTV kernel.
 //
-// Roles per CTA (cooperative launch, 1 CTA / SM, static round-robin tiles: CTA c handles
-// tiles c, c+G, c+2G, ... so every role can compute its own tile sequence):
-//   PRODUCER warp   : stage ring of STAGES slots; waits EMPTY[s], issues the TMA bulk copies of
-//                     tile k into slot k % STAGES (or fills a partial tail tile itself), and
-//                     publishes the previous occupant's chain-job count with a release store.
-//   LOOKAHEAD warps : NLA warps, tile k handled by warp k % NLA as soon as FULL[s] fires:
-//                     count the tile's group heads, publish the aggregate, decoupled look-back,
-//                     base -> BASE[s].  They run ahead of the streamers by up to STAGES-1 tiles,
-//                     so a base is normally ready before the streamers need it.
-//   STREAMER warps  : w = vals * x[subk] (all gathers issued before any store), head bitmask,
-//                     then groups striped over threads: a group that ends inside tile+halo
-//                     within kShort rows is folded serially by one thread (__dadd_rn, row
-//                     order: the reference's exact sequence, _ckernels.pyx:274-294) and written
-//                     at base + local id once BASE[s] fires; longer / tile-crossing groups become
-//                     per-tile chain jobs (no global atomics on this path).  Then EMPTY[s].
-//   CHAIN warps     : take tiles by ticket, wait for the tile's published job list, fold each
-//                     job's rows (L2-hot) in 256-row chunks: lane 0 folds from smem while the
-//                     next chunk is in flight.
-// Shared memory stays ~120 KB so L1 keeps the gathered vector x resident.
+// Cooperative launch, 1 CTA per SM, static round-robin tiles (CTA c: tiles c, c+G, c+2G, ...;
+// the CTA-local index k names them), 20 warps in five roles:
+//   PRODUCER  (1 warp)  : STAGES-slot TMA ring (cp.async.bulk of every column of tile k into slot
+//                         k % STAGES; partial tail tiles by plain loads); recycles a slot once its
+//                         pipe is done and publishes that tile's chain-job list (release store).
+//   LOOKAHEAD (kLookWarps) : tile k -> warp k % kLookWarps, up to RING tiles ahead of the pipes:
+//                         reads the tile's KEY columns straight from global memory (this also pulls
+//                         them into L2 for the TMA), counts group heads, publishes the tile aggregate
+//                         and runs the decoupled look-back -> base ring.  Bases are ready long before
+//                         the pipes need them, so the look-back latency never stalls the stream.
+//   PIPES     (2 x 4 warps) : pipe k % 2 processes tile k: w = vals * x[subk] (gathers issued before
+//                         any store), head bitmask, then each group headed in the tile is
+//                           short  (<= kShortFold rows, ends in tile+halo): folded at once by a thread;
+//                           medium (<= kShort rows, ends in tile+halo): queued in smem and then folded
+//                                   one group per lane, packed into as few warps as possible;
+//                           long / open (crosses the halo): a chain job (per-tile slot, no atomics).
+//                         Every fold is serial in row order with __dadd_rn -- the reference's exact
+//                         operation sequence (_ckernels.pyx:274-294) -- and outputs go to base + id.
+//   CHAIN     (kChainWarps) : take tiles by ticket, wait for the published job list, stream each
+//                         job's rows (L2-hot) in 256-row chunks, lane 0 folds while the next chunk is
+//                         in flight.
+// Shared memory ~150 KB, leaving L1 room for the gathered vector x.
 #pragma once
 
 #include "tk_stream.cuh"
 
 namespace tk {
 
-constexpr int kLookWarps = 3;  // 20 warps total: 5 per SMSP x 96 registers = one SMSP register file
-constexpr int kJobsPerTile = 16;  // 1 open group + TILE/(kShort+1) long closed groups (TILE <= 1024)
-constexpr int kWarpsTotal = 1 + kLookWarps + kStreamWarps + kChainWarps;
+constexpr int kLookWarps = 5;
+constexpr int kPipes = 2;
+constexpr int kPipeWarps = 4;
+constexpr int kChainW = 6;
+constexpr int kWarpsTotal = 1 + kLookWarps + kPipes * kPipeWarps + kChainW;  // 20
 constexpr int kThreadsV6 = kWarpsTotal * 32;
+constexpr int kRing = 12;        // look-ahead lead (tiles) / base ring slots
+constexpr int kShortFold = 8;    // in-place fold limit (rows) -- bounded SIMT divergence
+constexpr int kMaxMedium = 128;  // medium groups per tile (> TILE / (kShortFold + 1))
+constexpr int kJobsPerTile = 16; // 1 open group + TILE/(kShort+1) long closed groups (TILE <= 1024)
+static_assert(kWarpsTotal == 20, "5 warps per SMSP x 96 registers");
 
 template <int TILE, int HALO, int STAGES>
 constexpr size_t stream_smem_bytes(int ncol, int nk) {
-  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 * STAGES + (size_t)kChainWarps * kChunk * 8;
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 * STAGES + (size_t)kChainW * kChunk * 8 +
+         (size_t)kPipes * kMaxMedium * 8;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -43,16 +54,18 @@ __device__ __forceinline__ void st_release_u64g(unsigned long long* p, unsigned 
 }
 
 template <int SRC, int NK, int TILE, int HALO, int STAGES, int LBD>
-__global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warps x 96 regs fit an SM
+__global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warps x 96 regs = one SM
   constexpr int ROWS = TILE + HALO;
   constexpr int WORDS = ROWS / 32;
   constexpr int TWORDS = TILE / 32;
-  constexpr int ITER = (ROWS + 255) / 256;
-  constexpr int NSB = kStreamWarps * 32;
-  constexpr int GPT = TILE / NSB;  // max groups per streamer thread (nheads <= TILE)
+  constexpr int NPT = kPipeWarps * 32;       // threads per pipe
+  constexpr int ITER = (ROWS + NPT - 1) / NPT;
+  constexpr int GPT = TILE / NPT;            // group rounds per pipe thread (nheads <= TILE)
   constexpr int NKR = NK > 0 ? NK : kMaxKeep;
-  static_assert(ROWS % 32 == 0 && TILE % 256 == 0 && TILE <= 1024 && TWORDS <= 32, "tile geometry");
-  static_assert(1 + TILE / (kShort + 1) <= kJobsPerTile, "job slots per tile");
+  constexpr int LPR = TILE / 32;             // look-ahead rows per lane
+  static_assert(ROWS % 32 == 0 && TILE % NPT == 0 && TILE <= 1024 && TWORDS <= 32, "tile geometry");
+  static_assert(1 + TILE / (kShort + 1) <= kJobsPerTile && TILE / (kShortFold + 1) < kMaxMedium, "slots");
+  static_assert(STAGES >= kPipes + 1, "a slot per pipe plus one in flight");
   const SegParams& p = sp.s;
   const int nk = seg_nk<SRC, NK>(p);
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
@@ -60,13 +73,15 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
   const size_t stage_words = (size_t)ncol * ROWS + 2 * nk;  // + [nk][2] previous-row words
   long long* stage0 = reinterpret_cast<long long*>(smem_raw);
   double* chain_buf = reinterpret_cast<double*>(stage0 + stage_words * STAGES);
+  unsigned long long* s_med_all = reinterpret_cast<unsigned long long*>(chain_buf + kChainW * kChunk);
 
-  __shared__ __align__(8) uint64_t s_full[STAGES], s_empty[STAGES], s_based[STAGES];
-  __shared__ unsigned long long s_base[STAGES];
-  __shared__ unsigned long long s_jc[STAGES];  // (base << 8) | (njobs + 1) of the slot's tile
-  __shared__ unsigned int s_head[WORDS];
-  __shared__ int s_wpref[TWORDS + 1];
-  __shared__ int s_njobs;
+  __shared__ __align__(8) uint64_t s_full[STAGES], s_empty[STAGES], s_based[kRing];
+  __shared__ unsigned long long s_base[kRing];
+  __shared__ volatile long long s_ack[kRing];      // CTA-local tile whose base slot was consumed
+  __shared__ unsigned long long s_jc[STAGES];       // (base << 8) | (njobs + 1) of the slot's tile
+  __shared__ unsigned int s_head[kPipes][WORDS];
+  __shared__ int s_wpref[kPipes][TWORDS + 1];
+  __shared__ int s_njobs[kPipes], s_nmed[kPipes];
   __shared__ unsigned int s_flags;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -75,25 +90,30 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&s_empty[s], 1);
-      mbar_init(&s_based[s], 1);
     }
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&s_based[s], 1);
+      s_ack[s] = -1;
+    }
+    for (int q = 0; q < kPipes; ++q) s_njobs[q] = s_nmed[q] = 0;
     s_flags = 0;
-    s_njobs = 0;
   }
   __syncthreads();
   auto tile_of = [&](long long k) { return (long long)blockIdx.x + k * G; };
+  const long long kcount = sp.ntiles > blockIdx.x ? (sp.ntiles - blockIdx.x + G - 1) / G : 0;  // my tiles
 
   // =========================================== producer ===========================================
   if (warp == 0) {
-    for (long long k = 0;; ++k) {
-      const long long tile = tile_of(k);
+    // iteration k loads tile k and publishes the job list of tile k - STAGES (whose slot it reuses);
+    // the last STAGES iterations only drain
+    for (long long k = 0; k < kcount + STAGES; ++k) {
       const int s = (int)(k % STAGES);
       if (k >= STAGES) {
         mbar_wait(&s_empty[s], (unsigned)(((k / STAGES) - 1) & 1));
-        // publish the chain-job list of the tile that just left slot s
         if (lane == 0) st_release_u64g(sp.jcount + tile_of(k - STAGES), s_jc[s]);
       }
-      if (tile >= sp.ntiles) break;
+      if (k >= kcount) continue;
+      const long long tile = tile_of(k);
       const long long start = tile * TILE;
       const long long avail = min((long long)ROWS, p.n - start);
       long long* st = stage0 + stage_words * s;
@@ -143,51 +163,71 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
   // ========================================= look-ahead scan =========================================
   if (warp <= kLookWarps) {
     const int me = warp - 1;
-    for (long long k = me;; k += kLookWarps) {
+    for (long long k = me; k < kcount; k += kLookWarps) {
       const long long tile = tile_of(k);
-      if (tile >= sp.ntiles) break;
-      const int s = (int)(k % STAGES);
-      mbar_wait(&s_full[s], (unsigned)((k / STAGES) & 1));
-      const long long* st = stage0 + stage_words * s;
       const long long start = tile * TILE;
       const int cnt = (int)min((long long)TILE, p.n - start);
-      // heads among rows [0, cnt): row r is a head if its key differs from row r-1's
-      int agg = 0;
-      for (int r = lane; r < cnt; r += 32) {
-        bool head = (r == 0 && start == 0);
-        if (!head) {
+      // head flags of rows r = j*32 + lane (j < LPR), key columns read from global / L2
+      unsigned int hb = 0;  // bit j: row j*32+lane is a head
+#pragma unroll 1
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        const long long* col = p.key[c] + start;
+        long long prevcarry = (start > 0) ? __ldcg(col - 1) : 0;  // row start-1 (lane 0's predecessor)
+        constexpr int CH = LPR < 16 ? LPR : 16;  // rows per lane in flight (register budget)
+#pragma unroll 1
+        for (int j0 = 0; j0 < LPR; j0 += CH) {
+          long long v[CH];
 #pragma unroll
-          for (int c = 0; c < NKR; ++c) {
-            if (NK == 0 && c >= nk) break;
-            const long long va = st[(size_t)c * ROWS + r];
-            const long long vb = r ? st[(size_t)c * ROWS + r - 1] : st[(size_t)ncol * ROWS + 2 * c + 1];
-            head = head || va != vb;
+          for (int j = 0; j < CH; ++j) {
+            const int r = (j0 + j) * 32 + lane;
+            v[j] = r < cnt ? __ldcg(col + r) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const long long up = __shfl_up_sync(0xffffffffu, v[j], 1);
+            const long long last = __shfl_sync(0xffffffffu, v[j], 31);
+            const long long prev = lane == 0 ? prevcarry : up;
+            if (v[j] != prev) hb |= 1u << (j0 + j);
+            prevcarry = last;
           }
         }
-        agg += __popc(__ballot_sync(__activemask(), head)) * (lane == 0);
       }
-      agg = __shfl_sync(0xffffffffu, agg, 0);
+      if (start == 0 && lane == 0) hb |= 1u;
+      int agg = 0;
+#pragma unroll
+      for (int j = 0; j < LPR; ++j) {
+        const bool head = ((hb >> j) & 1u) && (j * 32 + lane < cnt);
+        agg += __popc(__ballot_sync(0xffffffffu, head));
+      }
       lookback_publish_agg<LBD>(p.status, tile, (unsigned long long)agg);
       const unsigned long long excl = lookback_wide<LBD>(p.status, tile, (unsigned long long)agg);
+      const int slot = (int)(k % kRing);
       if (lane == 0) {
-        s_base[s] = excl;
         if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
-        mbar_arrive(&s_based[s]);
+        while (k >= kRing && s_ack[slot] != k - kRing) __nanosleep(64);  // slot consumed?
+        s_base[slot] = excl;
+        mbar_arrive(&s_based[slot]);
       }
+      __syncwarp();
     }
     return;
   }
 
-  // ============================================ streamers ============================================
-  if (warp <= kLookWarps + kStreamWarps) {
-    const int t = tid - (1 + kLookWarps) * 32;  // 0..NSB-1
-    const int swarp = t >> 5;
+  // ============================================== pipes ==============================================
+  if (warp <= kLookWarps + kPipes * kPipeWarps) {
+    const int pw = warp - 1 - kLookWarps;  // 0 .. kPipes*kPipeWarps-1
+    const int pipe = pw / kPipeWarps;
+    const int t = (pw % kPipeWarps) * 32 + lane;  // thread within pipe
+    const int pwarp = t >> 5;
+    const int bar_id = 1 + pipe;
+    unsigned int* head = s_head[pipe];
+    int* wpref = s_wpref[pipe];
+    unsigned long long* med = s_med_all + pipe * kMaxMedium;
     unsigned int flags = 0;
-    for (long long k = 0;; ++k) {
+    for (long long k = pipe; k < kcount; k += kPipes) {
       const long long tile = tile_of(k);
-      if (tile >= sp.ntiles) break;
       const int s = (int)(k % STAGES);
-      const unsigned int par = (unsigned)((k / STAGES) & 1);
       long long* st = stage0 + stage_words * s;
       long long* s_key = st;
       double* s_a = reinterpret_cast<double*>(st + (size_t)nk * ROWS);
@@ -197,7 +237,7 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
       const int cnt = (int)min((long long)TILE, p.n - start);
       const int avail = (int)min((long long)ROWS, p.n - start);
       TKP_START(t_m);
-      mbar_wait(&s_full[s], par);
+      mbar_wait(&s_full[s], (unsigned)((k / STAGES) & 1));
       if (t == 0) TKP_ADD(0, t_m);
 
       // ---- w = vals * x[subk]: every gather in flight before any store ----
@@ -205,7 +245,7 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
         double xv[ITER], av[ITER];
 #pragma unroll
         for (int j = 0; j < ITER; ++j) {
-          const int r = j * NSB + t;
+          const int r = j * NPT + t;
           xv[j] = 0.0;
           av[j] = 0.0;
           if (r < avail) {
@@ -217,15 +257,15 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
         }
 #pragma unroll
         for (int j = 0; j < ITER; ++j) {
-          const int r = j * NSB + t;
+          const int r = j * NPT + t;
           if (r < avail) s_a[r] = __dmul_rn(av[j], xv[j]);
         }
       }
       // ---- head bitmask over tile + halo (striped rows) ----
 #pragma unroll
       for (int j = 0; j < ITER; ++j) {
-        const int r = j * NSB + t;
-        bool head = false;
+        const int r = j * NPT + t;
+        bool hd = false;
         if (r < avail) {
           int cmp = 0;
 #pragma unroll
@@ -239,18 +279,18 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
             }
           }
           if (r == 0 && start == 0) cmp = 1;
-          head = cmp != 0;
+          hd = cmp != 0;
           if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
         }
-        const unsigned int m = __ballot_sync(0xffffffffu, head);
-        const int wi = j * kStreamWarps + swarp;
-        if ((t & 31) == 0 && wi < WORDS) s_head[wi] = m;
+        const unsigned int m = __ballot_sync(0xffffffffu, hd);
+        const int wi = j * kPipeWarps + pwarp;
+        if (lane == 0 && wi < WORDS) head[wi] = m;
       }
-      named_bar(1, NSB);  // heads visible
-      if (swarp == 0) {   // exclusive popcount prefix of the tile's words
+      named_bar(bar_id, NPT);  // heads visible
+      if (pwarp == 0) {        // exclusive popcount prefix of the tile's words
         unsigned int w = 0;
         if (lane < TWORDS && lane * 32 < cnt) {
-          w = s_head[lane];
+          w = head[lane];
           if (lane * 32 + 32 > cnt) w &= (1u << (cnt - lane * 32)) - 1u;
         }
         int incl = __popc(w);
@@ -259,63 +299,61 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
           const int v = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += v;
         }
-        if (lane < TWORDS) s_wpref[lane] = incl - __popc(w);
-        if (lane == 31) s_wpref[TWORDS] = incl;  // head count of the tile
+        if (lane < TWORDS) wpref[lane] = incl - __popc(w);
+        if (lane == 31) wpref[TWORDS] = incl;
       }
-      named_bar(1, NSB);
+      named_bar(bar_id, NPT);
       if (t == 0) TKP_ADD(1, t_m);
       TKP_START(t_f);
 
-      // ---- groups striped over threads: fold short ones, queue the rest ----
-      const int nheads = s_wpref[TWORDS];
+      // ---- classify groups (striped over threads): fold short ones now ----
+      const int nheads = wpref[TWORDS];
       double gval[GPT];
       short grow[GPT];
 #pragma unroll
       for (int m = 0; m < GPT; ++m) {
-        const int li = t + m * NSB;
+        const int li = t + m * NPT;
         grow[m] = -1;
         gval[m] = 0.0;
         if (li >= nheads) continue;
-        // select: word holding the li-th head, then the bit inside it
-        int lo = 0, hi = TWORDS - 1;
+        int lo = 0, hi = TWORDS - 1;  // word holding the li-th head
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (s_wpref[mid] <= li) lo = mid;
+          if (wpref[mid] <= li) lo = mid;
           else hi = mid - 1;
         }
-        const unsigned int wd = s_head[lo];
-        const int r = lo * 32 + (int)__fns(wd, 0, li - s_wpref[lo] + 1);
+        const int r = lo * 32 + (int)__fns(head[lo], 0, li - wpref[lo] + 1);
         int end = avail;
         {
           const int q1 = r + 1;
           int wi = q1 >> 5;
-          unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
-          while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
+          unsigned int wb = (q1 < avail) ? (head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
+          while (wb == 0 && (wi + 1) * 32 < avail) wb = head[++wi];
           if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
         }
         const bool open = end == avail && start + avail < p.n;
-        if (!open && end - r <= kShort) {
+        const int len = end - r;
+        if (!open && len <= kShortFold) {
           gval[m] = fold_run(s_a, r + 1, end, s_a[r]);
           grow[m] = (short)r;
+        } else if (!open && len <= kShort) {
+          const int q = atomicAdd(&s_nmed[pipe], 1);
+          med[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
         } else {
-          const int j = atomicAdd(&s_njobs, 1);
+          const int j = atomicAdd(&s_njobs[pipe], 1);
           sp.jobs[tile * kJobsPerTile + j] = ((unsigned long long)r << 16) | (unsigned long long)li;
         }
       }
+      named_bar(bar_id, NPT);  // medium list complete
       if (t == 0) TKP_ADD(3, t_f);
       TKP_START(t_d);
-      mbar_wait(&s_based[s], par);
+      const int slot = (int)(k % kRing);
+      mbar_wait(&s_based[slot], (unsigned)((k / kRing) & 1));
+      const long long base = (long long)s_base[slot];
       if (t == 0) TKP_ADD(4, t_d);
       TKP_START(t_o);
-      const long long base = (long long)s_base[s];
-      unsigned int zeros = 0;
-#pragma unroll
-      for (int m = 0; m < GPT; ++m) {
-        const int r = grow[m];
-        if (r < 0) continue;
-        const long long g = base + t + m * NSB;
-        p.out_vals[g] = gval[m];
-        zeros += gval[m] == 0.0;
+      auto emit_short = [&](long long g, int r, double v) {
+        p.out_vals[g] = v;
         if constexpr (SRC == kSrcLinKey) {
           long long lin = s_key[r];
           long long* o = p.out_subs + g * p.out_nk;
@@ -331,32 +369,43 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 21 warp
             p.out_subs[g * p.out_nk + c] = s_key[c * ROWS + r];
           }
         }
+      };
+      unsigned int zeros = 0;
+      // medium groups: one per lane, packed into the first warps
+      const int nmed = s_nmed[pipe];
+      for (int q = t; q < nmed; q += NPT) {
+        const unsigned long long e = med[q];
+        const int li = (int)(e & 0xffff), r = (int)((e >> 16) & 0xffff), end = (int)(e >> 32);
+        const double v = fold_run(s_a, r + 1, end, s_a[r]);
+        zeros += v == 0.0;
+        emit_short(base + li, r, v);
+      }
+#pragma unroll
+      for (int m = 0; m < GPT; ++m) {
+        if (grow[m] < 0) continue;
+        zeros += gval[m] == 0.0;
+        emit_short(base + t + m * NPT, grow[m], gval[m]);
       }
       if (zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
-      named_bar(1, NSB);  // slot s consumed, job list complete
+      named_bar(bar_id, NPT);  // slot s consumed, job list complete
       if (t == 0) {
-        s_jc[s] = ((unsigned long long)base << 8) | (unsigned long long)(s_njobs + 1);
-        s_njobs = 0;
+        s_jc[s] = ((unsigned long long)base << 8) | (unsigned long long)(s_njobs[pipe] + 1);
+        s_njobs[pipe] = 0;
+        s_nmed[pipe] = 0;
+        s_ack[slot] = k;
         mbar_arrive(&s_empty[s]);
         TKP_ADD(5, t_o);
         TKP_COUNT(7, 1);
       }
     }
     if (flags) atomicOr(&s_flags, flags);
-    named_bar(1, NSB);
-    if (t == 0) {
-      if (s_flags) atomicOr(&p.ctr->flags, s_flags);
-      // the producer publishes each tile's job list when its slot is recycled; the last
-      // STAGES tiles of this CTA are never recycled, so publish them here
-      const long long kdone = (sp.ntiles - blockIdx.x + G - 1) / G;  // tiles of this CTA
-      for (long long k = max(0LL, kdone - STAGES); k < kdone; ++k)
-        st_release_u64g(sp.jcount + tile_of(k), s_jc[(int)(k % STAGES)]);
-    }
+    named_bar(bar_id, NPT);
+    if (t == 0 && s_flags) atomicOr(&p.ctr->flags, s_flags);
     return;
   }
 
   // ============================================= chain warps =============================================
-  double* cbuf = chain_buf + (size_t)(warp - (1 + kLookWarps + kStreamWarps)) * kChunk;
+  double* cbuf = chain_buf + (size_t)(warp - (1 + kLookWarps + kPipes * kPipeWarps)) * kChunk;
   while (true) {
     long long tile = 0;
     unsigned long long jc = 0;

@@ -374,10 +374,10 @@ int grid_for(long long n, int per_thread = 4) {
 
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  // geometry: 1 CTA per SM, a 3-slot TMA ring (~120 KB smem: L1 keeps x resident)
+  // geometry: 1 CTA per SM, a 4-slot TMA ring (2 pipes + 2 in flight; ~150 KB smem leaves L1 for x)
   constexpr int TILE = NK > 0 ? 1024 : 256;
   constexpr int HALO = 32;
-  constexpr int STAGES = 3;
+  constexpr int STAGES = 4;
   constexpr int LBD = 16;  // look-back window: 512 tiles per L2 round trip
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
