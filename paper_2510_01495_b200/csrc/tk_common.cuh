@@ -31,7 +31,7 @@ struct Counters {
   unsigned long long q_head;     // chain-job queue: next ticket handed to a chain warp
   unsigned long long q_tail;     // chain-job queue: jobs pushed so far
   unsigned int streamers_done;   // CTAs whose streamer warps have finished
-  unsigned int pad_;
+  unsigned int grab_ticket;      // stream kernel: tiles handed to CTAs in processing order
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -102,24 +102,30 @@ __device__ __forceinline__ unsigned long long lookback_wide(unsigned long long* 
       const long long t = look - (lane * D + i);
       s[i] = t >= 0 ? ld_relaxed(status + t) : kStPre;
     }
-    bool pending = true;
-    while (pending) {
-      bool mine = false;
+    // Only the entries nearer than the nearest inclusive prefix matter: wait until none of
+    // those is still unpublished (entries beyond the prefix may stay invalid).
+    int first_pre;
+    while (true) {
+      int fp = 1 << 30, fi = 1 << 30;
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) {
+        const unsigned long long f = s[i] >> 62;
+        if (f == 2) fp = lane * D + i;
+        if (f == 0) fi = lane * D + i;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fp = min(fp, __shfl_xor_sync(0xffffffffu, fp, o));
+        fi = min(fi, __shfl_xor_sync(0xffffffffu, fi, o));
+      }
+      if (fi > fp || fi == (1 << 30)) {
+        first_pre = fp;
+        break;
+      }
 #pragma unroll
       for (int i = 0; i < D; ++i)
-        if ((s[i] >> 62) == 0) {
-          s[i] = ld_relaxed(status + (look - (lane * D + i)));
-          mine = mine || (s[i] >> 62) == 0;
-        }
-      pending = __any_sync(0xffffffffu, mine);
+        if ((s[i] >> 62) == 0 && lane * D + i < fp) s[i] = ld_relaxed(status + (look - (lane * D + i)));
     }
-    // nearest prefix: smallest element index e = lane*D + i holding one
-    int first_pre = 1 << 30;
-#pragma unroll
-    for (int i = D - 1; i >= 0; --i)
-      if ((s[i] >> 62) == 2) first_pre = lane * D + i;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) first_pre = min(first_pre, __shfl_xor_sync(0xffffffffu, first_pre, o));
     unsigned long long v = 0;
 #pragma unroll
     for (int i = 0; i < D; ++i)

@@ -31,8 +31,8 @@ namespace tk {
 constexpr int kLookWarps = 5;
 constexpr int kPipes = 2;
 constexpr int kPipeWarps = 4;
-constexpr int kChainW = 6;
-constexpr int kWarpsTotal = 1 + kLookWarps + kPipes * kPipeWarps + kChainW;  // 20
+constexpr int kChainW = 5;
+constexpr int kWarpsTotal = 2 + kLookWarps + kPipes * kPipeWarps + kChainW;  // 20
 constexpr int kThreadsV6 = kWarpsTotal * 32;
 constexpr int kRing = 12;        // look-ahead lead (tiles) / base ring slots
 constexpr int kShortFold = 8;    // in-place fold limit (rows) -- bounded SIMT divergence
@@ -75,8 +75,9 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
   double* chain_buf = reinterpret_cast<double*>(stage0 + stage_words * STAGES);
   unsigned long long* s_med_all = reinterpret_cast<unsigned long long*>(chain_buf + kChainW * kChunk);
 
-  __shared__ __align__(8) uint64_t s_full[STAGES], s_empty[STAGES], s_based[kRing];
+  __shared__ __align__(8) uint64_t s_full[STAGES], s_empty[STAGES], s_based[kRing], s_tq[kRing];
   __shared__ unsigned long long s_base[kRing];
+  __shared__ long long s_tileq[kRing];             // tile id of CTA-local index k (-1: no more)
   __shared__ volatile long long s_ack[kRing];      // CTA-local tile whose base slot was consumed
   __shared__ unsigned long long s_jc[STAGES];       // (base << 8) | (njobs + 1) of the slot's tile
   __shared__ unsigned int s_head[kPipes][WORDS];
@@ -93,27 +94,74 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
     }
     for (int s = 0; s < kRing; ++s) {
       mbar_init(&s_based[s], 1);
+      mbar_init(&s_tq[s], 1);
       s_ack[s] = -1;
     }
     for (int q = 0; q < kPipes; ++q) s_njobs[q] = s_nmed[q] = 0;
     s_flags = 0;
   }
   __syncthreads();
-  auto tile_of = [&](long long k) { return (long long)blockIdx.x + k * G; };
-  const long long kcount = sp.ntiles > blockIdx.x ? (sp.ntiles - blockIdx.x + G - 1) / G : 0;  // my tiles
+  (void)G;
+  // tile id of CTA-local index k, once the ticketer has published it
+  auto tile_at = [&](long long k) {
+    mbar_wait(&s_tq[k % kRing], (unsigned)((k / kRing) & 1));
+    return s_tileq[k % kRing];
+  };
+
+  // ============================================ ticketer ============================================
+  // Hands tiles to this CTA in global processing order (dynamic: a slow CTA simply takes fewer),
+  // at most kRing ahead of the pipes.  After the first exhausted ticket it publishes enough -1
+  // sentinels for every role to stop.
+  if (warp == 0) {
+    if (lane == 0) {
+      long long kend = -1;
+      for (long long k = 0;; ++k) {
+        const int slot = (int)(k % kRing);
+        if (kend >= 0 && k > kend + kLookWarps) break;
+        if (k >= kRing)
+          while (s_ack[slot] != k - kRing) __nanosleep(64);  // the pipes are done with k - kRing
+        long long tile = -1;
+        if (kend < 0) {
+          tile = (long long)atomicAdd(&p.ctr->grab_ticket, 1u);
+          if (tile >= sp.ntiles) {
+            tile = -1;
+            kend = k;
+          }
+        }
+        s_tileq[slot] = tile;
+        mbar_arrive(&s_tq[slot]);
+      }
+    }
+    return;
+  }
 
   // =========================================== producer ===========================================
-  if (warp == 0) {
+  if (warp == 1) {
     // iteration k loads tile k and publishes the job list of tile k - STAGES (whose slot it reuses);
-    // the last STAGES iterations only drain
-    for (long long k = 0; k < kcount + STAGES; ++k) {
+    // after the last tile, STAGES more iterations only drain
+    long long kend = 1LL << 62;
+    long long prev_tiles[STAGES];
+#pragma unroll
+    for (int q = 0; q < STAGES; ++q) prev_tiles[q] = -1;
+    for (long long k = 0; k < kend + STAGES; ++k) {
       const int s = (int)(k % STAGES);
       if (k >= STAGES) {
         mbar_wait(&s_empty[s], (unsigned)(((k / STAGES) - 1) & 1));
-        if (lane == 0) st_release_u64g(sp.jcount + tile_of(k - STAGES), s_jc[s]);
+        long long pt = -1;
+#pragma unroll
+        for (int q = 0; q < STAGES; ++q)
+          if (q == s) pt = prev_tiles[q];
+        if (lane == 0) st_release_u64g(sp.jcount + pt, s_jc[s]);
       }
-      if (k >= kcount) continue;
-      const long long tile = tile_of(k);
+      if (k >= kend) continue;
+      const long long tile = tile_at(k);
+      if (tile < 0) {
+        kend = k;
+        continue;
+      }
+#pragma unroll
+      for (int q = 0; q < STAGES; ++q)
+        if (q == s) prev_tiles[q] = tile;
       const long long start = tile * TILE;
       const long long avail = min((long long)ROWS, p.n - start);
       long long* st = stage0 + stage_words * s;
@@ -161,10 +209,11 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
   }
 
   // ========================================= look-ahead scan =========================================
-  if (warp <= kLookWarps) {
-    const int me = warp - 1;
-    for (long long k = me; k < kcount; k += kLookWarps) {
-      const long long tile = tile_of(k);
+  if (warp <= 1 + kLookWarps) {
+    const int me = warp - 2;
+    for (long long k = me;; k += kLookWarps) {
+      const long long tile = tile_at(k);
+      if (tile < 0) break;
       const long long start = tile * TILE;
       const int cnt = (int)min((long long)TILE, p.n - start);
       // head flags of rows r = j*32 + lane (j < LPR), key columns read from global / L2
@@ -203,9 +252,8 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
       lookback_publish_agg<LBD>(p.status, tile, (unsigned long long)agg);
       const unsigned long long excl = lookback_wide<LBD>(p.status, tile, (unsigned long long)agg);
       const int slot = (int)(k % kRing);
-      if (lane == 0) {
+      if (lane == 0) {  // (slot k % kRing is free: the ticketer waited for its ack before issuing k)
         if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
-        while (k >= kRing && s_ack[slot] != k - kRing) __nanosleep(64);  // slot consumed?
         s_base[slot] = excl;
         mbar_arrive(&s_based[slot]);
       }
@@ -215,8 +263,8 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
   }
 
   // ============================================== pipes ==============================================
-  if (warp <= kLookWarps + kPipes * kPipeWarps) {
-    const int pw = warp - 1 - kLookWarps;  // 0 .. kPipes*kPipeWarps-1
+  if (warp <= 1 + kLookWarps + kPipes * kPipeWarps) {
+    const int pw = warp - 2 - kLookWarps;  // 0 .. kPipes*kPipeWarps-1
     const int pipe = pw / kPipeWarps;
     const int t = (pw % kPipeWarps) * 32 + lane;  // thread within pipe
     const int pwarp = t >> 5;
@@ -225,8 +273,9 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
     int* wpref = s_wpref[pipe];
     unsigned long long* med = s_med_all + pipe * kMaxMedium;
     unsigned int flags = 0;
-    for (long long k = pipe; k < kcount; k += kPipes) {
-      const long long tile = tile_of(k);
+    for (long long k = pipe;; k += kPipes) {
+      const long long tile = tile_at(k);
+      if (tile < 0) break;
       const int s = (int)(k % STAGES);
       long long* st = stage0 + stage_words * s;
       long long* s_key = st;
@@ -405,7 +454,7 @@ __global__ void __maxnreg__(96) ttv_stream_kernel(StreamParams sp) {  // 20 warp
   }
 
   // ============================================= chain warps =============================================
-  double* cbuf = chain_buf + (size_t)(warp - (1 + kLookWarps + kPipes * kPipeWarps)) * kChunk;
+  double* cbuf = chain_buf + (size_t)(warp - (2 + kLookWarps + kPipes * kPipeWarps)) * kChunk;
   while (true) {
     long long tile = 0;
     unsigned long long jc = 0;
