@@ -1,0 +1,343 @@
+// tk_tile_kernel.cuh -- sparse-result TTV: one compact CTA per tile, many CTAs per SM.
+//
+// Per CTA (256 threads, TILE rows + HALO look-ahead rows, tiles handed out in launch order):
+//   1. thread 0 takes a ticket and stages every column of the tile into shared memory with 1-D
+//      TMA bulk copies (cp.async.bulk, one mbarrier); partial tail tiles use plain loads;
+//   2. w = vals * x[subk] with all gathers in flight before any store (x stays L1-resident: the
+//      CTA needs ~37 KB of shared memory, so four CTAs per SM still leave L1 ~100 KB), and the
+//      head bitmask of the kept-key stream;
+//   3. warp 0: popcount prefix, publish the tile aggregate, decoupled look-back (its latency
+//      overlaps the folds of warps 1-7, and other CTAs on the SM keep the memory pipe busy);
+//      warps 1-7: every group headed in the tile is classified -- short groups are folded at once,
+//      other groups that close inside tile+halo are folded one group per thread from a packed
+//      list, the (at most one) group that runs past the halo is finished cooperatively at the end;
+//      every fold is serial in row order with __dadd_rn: the reference's exact operation sequence
+//      (_ckernels.pyx:274-294), hence bit-identical values;
+//   4. coalesced writes of (key, value) at base + local id; the spilling group last.
+#pragma once
+
+#include "tk_stream.cuh"
+
+namespace tk {
+
+constexpr int kTileThreads = 256;
+constexpr int kTileShort = 8;  // folded inline by the classifying thread
+
+template <int TILE>
+constexpr int tile_list_cap() {  // closed groups longer than kTileShort rows per tile (+ slack)
+  return ((TILE / (kTileShort + 1) + 8) + 15) & ~15;
+}
+
+// stage columns + previous-row words + head-row ids + long-group list (+ value area for the
+// precomputed-w sources, which have no subk column to reuse)
+template <int TILE, int HALO>
+constexpr size_t tile_smem_bytes(int ncol, int nk) {
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)TILE * 2 + (size_t)tile_list_cap<TILE>() * 8;
+}
+
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int SRC, int NK, int TILE, int HALO>
+__global__ void __launch_bounds__(kTileThreads, 4) ttv_tile_kernel(SegParams p) {
+  constexpr int ROWS = TILE + HALO;
+  constexpr int WORDS = ROWS / 32;
+  constexpr int TWORDS = TILE / 32;
+  constexpr int ITER = (ROWS + kTileThreads - 1) / kTileThreads;
+  constexpr int NKR = NK > 0 ? NK : kMaxKeep;
+  constexpr int NCLS = kTileThreads - 32;  // classifier threads (warps 1-7)
+  static_assert(ROWS % 32 == 0 && TWORDS <= 32 && TILE % 32 == 0, "tile geometry");
+  const int nk = seg_nk<SRC, NK>(p);
+  const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  long long* st = reinterpret_cast<long long*>(smem_raw);
+  long long* s_key = st;
+  double* s_a = reinterpret_cast<double*>(st + (size_t)nk * ROWS);
+  long long* s_subk = st + (size_t)(nk + 1) * ROWS;
+  long long* s_prev2 = st + (size_t)ncol * ROWS;
+  // folded values by local id reuse the subk column (free once w is formed); for the
+  // precomputed-w sources there is no subk column, so they get their own area
+  short* s_row = reinterpret_cast<short*>(s_prev2 + 2 * nk);
+  unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_row + TILE);
+  double* s_val =
+      SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : reinterpret_cast<double*>(s_list + tile_list_cap<TILE>());
+
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ long long s_tile;
+  __shared__ int s_bulk;
+  __shared__ unsigned int s_head[WORDS];
+  __shared__ int s_wpref[TWORDS + 1];
+  __shared__ unsigned long long s_base;
+  __shared__ int s_nlist, s_open_li, s_open_r, s_end;
+  __shared__ unsigned int s_flags, s_zeros;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const long long tile = (long long)atomicAdd(&p.ctr->tile_ticket, 1u);
+    s_tile = tile;
+    s_nlist = 0;
+    s_open_li = -1;
+    s_flags = 0;
+    s_zeros = 0;
+    const long long start = tile * TILE;
+    const long long avail = min((long long)ROWS, p.n - start);
+    const bool bulk = p.bulk_ok && avail == ROWS;
+    s_bulk = bulk;
+    if (bulk) {
+      mbar_init(&s_bar, 1);
+      const uint32_t bytes = ROWS * 8u;
+      mbar_arrive_expect_tx(&s_bar, bytes * ncol + (start > 0 ? 16u * nk : 0u));
+      for (int c = 0; c < nk; ++c) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(st + (size_t)c * ROWS)),
+            "l"(p.key[c] + start), "r"(bytes), "r"(smem_u32(&s_bar))
+            : "memory");
+        if (start > 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                  smem_u32(s_prev2 + 2 * c)),
+              "l"(p.key[c] + start - 2), "r"(smem_u32(&s_bar))
+              : "memory");
+      }
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(s_a)),
+          "l"(p.a + start), "r"(bytes), "r"(smem_u32(&s_bar))
+          : "memory");
+      if constexpr (SRC == kSrcRaw)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(s_subk)),
+            "l"(p.subk + start), "r"(bytes), "r"(smem_u32(&s_bar))
+            : "memory");
+    }
+  }
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long start = tile * TILE;
+  const int cnt = (int)min((long long)TILE, p.n - start);
+  const int avail = (int)min((long long)ROWS, p.n - start);
+  if (s_bulk) {
+    mbar_wait(&s_bar, 0);
+  } else {
+    for (int r = tid; r < avail; r += kTileThreads) {
+      for (int c = 0; c < nk; ++c) s_key[(size_t)c * ROWS + r] = p.key[c][start + r];
+      s_a[r] = p.a[start + r];
+      if constexpr (SRC == kSrcRaw) s_subk[r] = p.subk[start + r];
+    }
+    if (tid < nk && start > 0) s_prev2[2 * tid + 1] = p.key[tid][start - 1];
+    __syncthreads();
+  }
+
+  // ---- w = vals * x[subk] (all gathers in flight first) and head flags ----
+  unsigned int flags = 0;
+  if constexpr (SRC == kSrcRaw) {
+    double xv[ITER], av[ITER];
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int r = j * kTileThreads + tid;
+      xv[j] = 0.0;
+      av[j] = 0.0;
+      if (r < avail) {
+        const long long idx = s_subk[r];
+        av[j] = s_a[r];
+        if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+        else xv[j] = __ldg(p.x + idx);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int r = j * kTileThreads + tid;
+      if (r < avail) s_a[r] = __dmul_rn(av[j], xv[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int r = j * kTileThreads + tid;
+    bool hd = false;
+    if (r < avail) {
+      int cmp = 0;
+#pragma unroll
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        const long long va = s_key[c * ROWS + r];
+        const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
+        if (va != vb) {
+          cmp = va < vb ? -1 : 1;
+          break;
+        }
+      }
+      if (r == 0 && start == 0) cmp = 1;
+      hd = cmp != 0;
+      if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
+    }
+    const unsigned int m = __ballot_sync(0xffffffffu, hd);
+    const int wi = j * (kTileThreads / 32) + warp;
+    if (lane == 0 && wi < WORDS) s_head[wi] = m;
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- popcount prefix, aggregate, decoupled look-back ----
+    unsigned int w = 0;
+    if (lane < TWORDS && lane * 32 < cnt) {
+      w = s_head[lane];
+      if (lane * 32 + 32 > cnt) w &= (1u << (cnt - lane * 32)) - 1u;
+    }
+    int incl = __popc(w);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane < TWORDS) s_wpref[lane] = incl - __popc(w);
+    const int agg = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0) s_wpref[TWORDS] = agg;
+    __syncwarp();
+    named_arrive(1, kTileThreads);  // local ids ready for the classifiers
+    lookback_publish_agg<8>(p.status, tile, (unsigned long long)agg);
+    const unsigned long long excl = lookback_wide<8>(p.status, tile, (unsigned long long)agg);
+    if (lane == 0) {
+      s_base = excl;
+      if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
+    }
+  } else {
+    named_bar(1, kTileThreads);
+    // ---- classify every group headed in the tile (striped over warps 1-7) ----
+    const int nheads = s_wpref[TWORDS];
+    const int tc = tid - 32;
+    for (int li = tc; li < nheads; li += NCLS) {
+      int lo = 0, hi = TWORDS - 1;  // word holding the li-th head
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_wpref[mid] <= li) lo = mid;
+        else hi = mid - 1;
+      }
+      const int r = lo * 32 + (int)__fns(s_head[lo], 0, li - s_wpref[lo] + 1);
+      int end = avail;
+      {
+        const int q1 = r + 1;
+        int wi = q1 >> 5;
+        unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
+        while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
+        if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
+      }
+      const bool open = end == avail && start + avail < p.n;
+      if (open) {
+        s_open_li = li;
+        s_open_r = r;
+        s_row[li] = -1;
+      } else if (end - r <= kTileShort) {
+        s_val[li] = fold_run(s_a, r + 1, end, s_a[r]);
+        s_row[li] = (short)r;
+      } else {
+        s_row[li] = (short)r;
+        const int q = atomicAdd(&s_nlist, 1);
+        s_list[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
+      }
+    }
+    named_bar(2, NCLS);
+    // ---- longer closed groups: one per thread, packed into the first warps ----
+    const int nl = s_nlist;
+    for (int q = tc; q < nl; q += NCLS) {
+      const unsigned long long e = s_list[q];
+      const int li = (int)(e & 0xffff), r = (int)((e >> 16) & 0xffff), end = (int)(e >> 32);
+      s_val[li] = fold_run(s_a, r + 1, end, s_a[r]);
+    }
+  }
+  __syncthreads();
+
+  // ---- coalesced output of every group closed inside the stage ----
+  const long long base = (long long)s_base;
+  const int nheads = s_wpref[TWORDS];
+  unsigned int zeros = 0;
+  for (int li = tid; li < nheads; li += kTileThreads) {
+    const int r = s_row[li];
+    if (r < 0) continue;
+    const double v = s_val[li];
+    const long long g = base + li;
+    p.out_vals[g] = v;
+    zeros += v == 0.0;
+    if constexpr (SRC == kSrcLinKey) {
+      long long lin = s_key[r];
+      long long* o = p.out_subs + g * p.out_nk;
+      for (int q = p.out_nk - 1; q >= 0; --q) {
+        const long long dm = p.dims[q];
+        o[q] = lin % dm;
+        lin /= dm;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        p.out_subs[g * p.out_nk + c] = s_key[c * ROWS + r];
+      }
+    }
+  }
+  if (zeros) atomicAdd(&s_zeros, zeros);
+  const int open_li = s_open_li;
+  if (open_li < 0) {
+    __syncthreads();
+    if (tid == 0) {
+      if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
+      if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+    }
+    return;
+  }
+
+  // ---- the group that runs past the halo: stream its rows in 1024-row chunks (L2-hot: the next
+  //      tiles' CTAs are reading them), thread 0 folds from smem ----
+  const int r0 = s_open_r;
+  long long gk[NKR];
+#pragma unroll
+  for (int c = 0; c < NKR; ++c)
+    if (NK > 0 || c < nk) gk[c] = s_key[c * ROWS + r0];
+  double acc = 0.0;  // meaningful in thread 0, which does every fold of this group
+  if (tid == 0) acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
+  __syncthreads();  // the stage is free from here on: reuse it as the chunk buffer
+  double* cb = reinterpret_cast<double*>(st);
+  constexpr int CH = 1024;
+  for (long long pos = start + avail; pos < p.n; pos += CH) {
+    if (tid == 0) s_end = CH;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < CH / kTileThreads; ++j) {
+      const int r = j * kTileThreads + tid;
+      const long long row = pos + r;
+      bool same = row < p.n;
+      double w = 0.0;
+      if (same) {
+#pragma unroll
+        for (int c = 0; c < NKR; ++c)
+          if (NK > 0 || c < nk) same = same && __ldcg(p.key[c] + row) == gk[c];
+        w = __ldcg(p.a + row);
+        if constexpr (SRC == kSrcRaw) {
+          const long long idx = __ldcg(p.subk + row);
+          w = (idx < 0 || idx >= p.nx) ? 0.0 : __dmul_rn(w, __ldg(p.x + idx));
+        }
+      }
+      cb[r] = w;
+      if (!same) atomicMin(&s_end, r);
+    }
+    __syncthreads();
+    const int end = s_end;
+    if (tid == 0) acc = fold_run(cb, 0, end, acc);
+    if (end < CH) break;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const long long g = base + open_li;
+    long long kv[NKR];
+#pragma unroll
+    for (int c = 0; c < NKR; ++c)
+      if (NK > 0 || c < nk) kv[c] = gk[c];
+    seg_emit<SRC>(p, g, kv, acc);
+    if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
+    if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+  }
+}
+
+}  // namespace tk

@@ -23,7 +23,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "tk_host.h"
-#include "tk_stream_kernel.cuh"
+#include "tk_tile_kernel.cuh"
 #include "tk_ttv_kernels.cuh"
 
 namespace tk {
@@ -374,66 +374,29 @@ int grid_for(long long n, int per_thread = 4) {
 
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  // geometry: 1 CTA per SM, a 4-slot TMA ring (2 pipes + 2 in flight; ~150 KB smem leaves L1 for x)
-  constexpr int TILE = NK > 0 ? 1024 : 256;
+  // one CTA per tile, four CTAs per SM (~37 KB shared memory each: L1 keeps x resident)
+  constexpr int TILE = NK > 0 ? 1024 : 512;
   constexpr int HALO = 32;
-  constexpr int STAGES = 4;
-  constexpr int LBD = 16;  // look-back window: 512 tiles per L2 round trip
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
-  const size_t smem = stream_smem_bytes<TILE, HALO, STAGES>(ncol, nk);
-  auto kern = ttv_stream_kernel<SRC, NK, TILE, HALO, STAGES, LBD>;
+  const size_t smem = tile_smem_bytes<TILE, HALO>(ncol, nk) + (SRC == kSrcRaw ? 0 : (size_t)TILE * 8);
+  auto kern = ttv_tile_kernel<SRC, NK, TILE, HALO>;
   set_smem_once(kern, smem);
-  int per_sm = 0;
-  TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsV6, smem));
-  if (per_sm < 1) return fail(TK_EARG, "ttv: stream kernel does not fit on an SM");
-  per_sm = 1;
   const long long ntiles = (p.n + TILE - 1) / TILE;
-  // scratch: look-back status | counters | job counts (zeroed per call) | job slots
   const size_t status_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
-  const size_t jc_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
   DevBuf scratch;
-  if (int rc = scratch.alloc(status_b + 256 + jc_b + (size_t)ntiles * kJobsPerTile * 8, st)) return rc;
+  if (int rc = scratch.alloc(status_b + 256, st)) return rc;
   char* b = scratch.as<char>();
   p.status = reinterpret_cast<unsigned long long*>(b);
   p.ctr = reinterpret_cast<Counters*>(b + status_b);
-  StreamParams sp{};
-  sp.s = p;
-  sp.jcount = reinterpret_cast<unsigned long long*>(b + status_b + 256);
-  sp.jobs = reinterpret_cast<StreamJob*>(b + status_b + 256 + jc_b);
-  sp.ntiles = ntiles;
-  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256 + jc_b, st));
-  const unsigned grid = (unsigned)(per_sm * num_sms());
-  DevBuf prof;
-  const bool profile = getenv("TK_STREAM_PROFILE") != nullptr;
-  if (profile) {
-    if (int rc = prof.alloc((size_t)grid * 16 * 8, st)) return rc;
-    TK_CUDA(cudaMemsetAsync(prof.get(), 0, (size_t)grid * 16 * 8, st));
-    sp.prof = prof.as<unsigned long long>();
-  }
-  void* args[] = {&sp};
+  TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
   ktimer_begin(st);
-  TK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreadsV6), args, smem, st));
+  kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();
+  TK_CUDA(cudaGetLastError());
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
-  if (profile) {
-    std::vector<unsigned long long> h((size_t)grid * 16);
-    TK_CUDA(cudaMemcpy(h.data(), prof.get(), h.size() * 8, cudaMemcpyDeviceToHost));
-    static const char* names[16] = {"tma_wait", "head(+wait)", "bar_B", "folds", "wait_base", "output",
-                                    "bar_A", "tiles", "scan_idle", "scan_lookback", "chain_idle", "chain_busy",
-                                    "chain_jobs", "chain_rows", "", ""};
-    fprintf(stderr, "[tk stream profile] grid=%u ntiles=%lld (per-CTA mean; cycles->us at 1.965 GHz)\n", grid,
-            ntiles);
-    for (int k = 0; k < 14; ++k) {
-      double sum = 0;
-      for (unsigned c = 0; c < grid; ++c) sum += (double)h[(size_t)c * 16 + k];
-      const double mean = sum / grid;
-      if (k == 7 || k == 12 || k == 13) fprintf(stderr, "  %-14s %14.1f (total %.0f)\n", names[k], mean, sum);
-      else fprintf(stderr, "  %-14s %14.1f us\n", names[k], mean / 1965.0);
-    }
-  }
   return TK_OK;
 }
 
