@@ -20,7 +20,7 @@
 
 namespace tk {
 
-constexpr int kTileThreads = 256;
+constexpr int kTileThreads = 128;  // threads per CTA (8 CTAs per SM)
 constexpr int kTileShort = 8;  // folded inline by the classifying thread
 
 template <int TILE>
@@ -40,7 +40,7 @@ __device__ __forceinline__ void named_arrive(int id, int threads) {
 }
 
 template <int SRC, int NK, int TILE, int HALO>
-__global__ void __launch_bounds__(kTileThreads, 4) ttv_tile_kernel(SegParams p) {
+__global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) {
   constexpr int ROWS = TILE + HALO;
   constexpr int WORDS = ROWS / 32;
   constexpr int TWORDS = TILE / 32;
@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) ttv_tile_kernel(SegParams p) 
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    const long long tile = (long long)atomicAdd(&p.ctr->tile_ticket, 1u);
+    // blocks are dispatched in index order, so every predecessor tile is resident or done
+    // when this one looks back (the single-pass scan convention)
+    const long long tile = (long long)blockIdx.x;
     s_tile = tile;
     s_nlist = 0;
     s_open_li = -1;
@@ -198,8 +200,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) ttv_tile_kernel(SegParams p) 
     if (lane == 0) s_wpref[TWORDS] = agg;
     __syncwarp();
     named_arrive(1, kTileThreads);  // local ids ready for the classifiers
-    lookback_publish_agg<8>(p.status, tile, (unsigned long long)agg);
-    const unsigned long long excl = lookback_wide<8>(p.status, tile, (unsigned long long)agg);
+    lookback_publish_agg<16>(p.status, tile, (unsigned long long)agg);
+    const unsigned long long excl = lookback_wide<16>(p.status, tile, (unsigned long long)agg);
     if (lane == 0) {
       s_base = excl;
       if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) ttv_tile_kernel(SegParams p) 
   if (tid == 0) acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
   __syncthreads();  // the stage is free from here on: reuse it as the chunk buffer
   double* cb = reinterpret_cast<double*>(st);
-  constexpr int CH = 1024;
+  constexpr int CH = 4 * kTileThreads;
   for (long long pos = start + avail; pos < p.n; pos += CH) {
     if (tid == 0) s_end = CH;
     __syncthreads();

@@ -374,8 +374,8 @@ int grid_for(long long n, int per_thread = 4) {
 
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
-  // one CTA per tile, four CTAs per SM (~37 KB shared memory each: L1 keeps x resident)
-  constexpr int TILE = NK > 0 ? 1024 : 512;
+  // one CTA per tile, eight CTAs per SM (~19 KB shared memory each: L1 keeps x resident)
+  constexpr int TILE = NK > 0 ? 512 : 256;
   constexpr int HALO = 32;
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
