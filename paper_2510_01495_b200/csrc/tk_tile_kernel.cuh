@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   __shared__ unsigned int s_flags, s_zeros;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long t_0 = TKT_NOW();
   if (tid == 0) {
     // blocks are dispatched in index order, so every predecessor tile is resident or done
     // when this one looks back (the single-pass scan convention)
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   const int avail = (int)min((long long)ROWS, p.n - start);
   if (s_bulk) {
     mbar_wait(&s_bar, 0);
+    if (tid == 0) TKT_ADD(0, TKT_NOW() - t_0);
   } else {
     for (int r = tid; r < avail; r += kTileThreads) {
       for (int c = 0; c < nk; ++c) s_key[(size_t)c * ROWS + r] = p.key[c][start + r];
@@ -181,6 +183,8 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   }
   if (flags) atomicOr(&s_flags, flags);
   __syncthreads();
+  const long long t_2 = TKT_NOW();
+  if (tid == 0) TKT_ADD(1, t_2 - t_0);
 
   if (warp == 0) {
     // ---- popcount prefix, aggregate, decoupled look-back ----
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     if (lane == 0) {
       s_base = excl;
       if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
+      TKT_ADD(2, TKT_NOW() - t_2);
     }
   } else {
     named_bar(1, kTileThreads);
@@ -251,6 +256,8 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     }
   }
   __syncthreads();
+  const long long t_3 = TKT_NOW();
+  if (tid == 0) TKT_ADD(3, t_3 - t_2);
 
   // ---- coalesced output of every group closed inside the stage ----
   const long long base = (long long)s_base;
@@ -281,14 +288,20 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   }
   if (zeros) atomicAdd(&s_zeros, zeros);
   const int open_li = s_open_li;
+  if (tid == 0) {
+    TKT_ADD(4, TKT_NOW() - t_3);
+    TKT_ADD(6, 1);
+  }
   if (open_li < 0) {
     __syncthreads();
     if (tid == 0) {
       if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
       if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+      TKT_ADD(9, TKT_NOW() - t_0);
     }
     return;
   }
+  const long long t_4 = TKT_NOW();
 
   // ---- the group that runs past the halo: stream its rows in 1024-row chunks (L2-hot: the next
   //      tiles' CTAs are reading them), thread 0 folds from smem ----
@@ -339,6 +352,10 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     seg_emit<SRC>(p, g, kv, acc);
     if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
     if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+    const long long t_5 = TKT_NOW();
+    TKT_ADD(5, t_5 - t_4);
+    TKT_ADD(7, 1);
+    TKT_ADD(9, t_5 - t_0);
   }
 }
 

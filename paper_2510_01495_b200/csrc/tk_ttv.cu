@@ -390,6 +390,13 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   p.status = reinterpret_cast<unsigned long long*>(b);
   p.ctr = reinterpret_cast<Counters*>(b + status_b);
   TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
+  DevBuf prof;
+  const bool profile = getenv("TK_TILE_PROFILE") != nullptr;
+  if (profile) {
+    if (int rc = prof.alloc(16 * 8, st)) return rc;
+    TK_CUDA(cudaMemsetAsync(prof.get(), 0, 16 * 8, st));
+    p.prof = prof.as<unsigned long long>();
+  }
   ktimer_begin(st);
   kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(p);
   ktimer_end(st);
@@ -397,6 +404,17 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   TK_CUDA(cudaGetLastError());
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
+  if (profile) {
+    unsigned long long h[16];
+    TK_CUDA(cudaMemcpy(h, prof.get(), sizeof h, cudaMemcpyDeviceToHost));
+    const double nt = (double)std::max(1ull, h[6]), ns = (double)std::max(1ull, h[7]);
+    fprintf(stderr,
+            "[tk tile profile] tiles=%llu spills=%llu | per tile (us): data %.2f  w+heads %.2f  lookback %.2f  "
+            "folds+lb %.2f  output %.2f  life %.2f | per spill: %.2f us\n",
+            h[6], h[7], h[0] / nt / 1965.0, (h[1] - h[0]) / nt / 1965.0, h[2] / nt / 1965.0, h[3] / nt / 1965.0,
+            h[4] / nt / 1965.0, h[9] / nt / 1965.0, h[5] / ns / 1965.0);
+    p.prof = nullptr;
+  }
   return TK_OK;
 }
 

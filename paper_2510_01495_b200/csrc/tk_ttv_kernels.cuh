@@ -50,7 +50,15 @@ struct SegParams {
   unsigned long long* status;        // look-back words, one per tile (zeroed)
   Counters* ctr;
   int bulk_ok;                       // all stream pointers 16-byte aligned
+  unsigned long long* prof;          // optional phase counters (TK_TILE_PROFILE=1), else null
 };
+
+// development instrumentation: clock64 deltas summed over CTAs (off unless p.prof != null)
+#define TKT_NOW() (p.prof ? clock64() : 0LL)
+#define TKT_ADD(slot, v)                                                   \
+  do {                                                                     \
+    if (p.prof) atomicAdd(p.prof + (slot), (unsigned long long)(v));       \
+  } while (0)
 
 template <int kItems>
 struct SegTile {
