@@ -39,6 +39,67 @@ __device__ __forceinline__ void named_arrive(int id, int threads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// The sequential scanner (block 0 of the launch, warp 0): turns published tile aggregates into
+// inclusive prefixes, in order, as fast as they appear.  Each round it takes the longest run of
+// already-published aggregates in the next 32*D tiles (one L2 round trip), scans it, publishes the
+// prefixes and advances.  A tile therefore waits ~one round trip after its own aggregate, and
+// polls only its own status word -- no wide look-back windows hammering L2.
+template <int D>
+__device__ void tile_scanner(unsigned long long* status, long long ntiles) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long carry = 0;
+  long long w = 0;
+  while (w < ntiles) {
+    unsigned long long v[D];
+    int my_first_missing = D;  // first unpublished element of this lane
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const long long t = w + lane * D + i;
+      v[i] = t < ntiles ? ld_relaxed(status + t) : (kStAgg | 0ull);
+      if ((v[i] >> 62) == 0 && my_first_missing == D) my_first_missing = i;
+    }
+    // global position of the first unpublished tile in the window
+    int first = my_first_missing < D ? lane * D + my_first_missing : 32 * D;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if (first == 0) {
+      __nanosleep(200);
+      continue;
+    }
+    // inclusive scan of the published run [0, first)
+    unsigned long long run = 0, loc[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int e = lane * D + i;
+      run += (e < first) ? (v[i] & kStVal) : 0ull;
+      loc[i] = run;
+    }
+    unsigned long long incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long up = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += up;
+    }
+    const unsigned long long excl_lane = carry + incl - run;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int e = lane * D + i;
+      const long long t = w + e;
+      if (e < first && t < ntiles) st_relaxed(status + t, kStPre | (excl_lane + loc[i]));
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+    w += first;
+  }
+}
+
+// A tile's exclusive prefix once the scanner has published it (tile 0: 0).
+__device__ __forceinline__ unsigned long long tile_wait_prefix(unsigned long long* status, long long tile,
+                                                               unsigned long long agg) {
+  unsigned long long s;
+  while (((s = ld_relaxed(status + tile)) >> 62) != 2) __nanosleep(128);
+  return (s & kStVal) - agg;
+}
+
 template <int SRC, int NK, int TILE, int HALO>
 __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) {
   constexpr int ROWS = TILE + HALO;
@@ -73,11 +134,15 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   __shared__ unsigned int s_flags, s_zeros;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
+    if (warp == 0) tile_scanner<16>(p.status, (p.n + TILE - 1) / TILE);
+    return;
+  }
   const long long t_0 = TKT_NOW();
   if (tid == 0) {
     // blocks are dispatched in index order, so every predecessor tile is resident or done
-    // when this one looks back (the single-pass scan convention)
-    const long long tile = (long long)blockIdx.x;
+    // (the single-pass scan convention); block b handles tile b - 1
+    const long long tile = (long long)blockIdx.x - 1;
     s_tile = tile;
     s_nlist = 0;
     s_open_li = -1;
@@ -204,9 +269,9 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     if (lane == 0) s_wpref[TWORDS] = agg;
     __syncwarp();
     named_arrive(1, kTileThreads);  // local ids ready for the classifiers
-    lookback_publish_agg<16>(p.status, tile, (unsigned long long)agg);
-    const unsigned long long excl = lookback_wide<16>(p.status, tile, (unsigned long long)agg);
     if (lane == 0) {
+      st_relaxed(p.status + tile, kStAgg | (unsigned long long)agg);
+      const unsigned long long excl = tile_wait_prefix(p.status, tile, (unsigned long long)agg);
       s_base = excl;
       if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
       TKT_ADD(2, TKT_NOW() - t_2);
@@ -318,23 +383,30 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   for (long long pos = start + avail; pos < p.n; pos += CH) {
     if (tid == 0) s_end = CH;
     __syncthreads();
+    constexpr int RPT = CH / kTileThreads;
+    long long kv[RPT][NKR], sk[RPT];
+    double av[RPT], xv[RPT];
 #pragma unroll
-    for (int j = 0; j < CH / kTileThreads; ++j) {
+    for (int j = 0; j < RPT; ++j) {  // every load of the chunk in flight at once
+      const long long row = pos + j * kTileThreads + tid;
+      const bool ok = row < p.n;
+#pragma unroll
+      for (int c = 0; c < NKR; ++c)
+        if (NK > 0 || c < nk) kv[j][c] = ok ? __ldcg(p.key[c] + row) : 0;
+      av[j] = ok ? __ldcg(p.a + row) : 0.0;
+      sk[j] = (SRC == kSrcRaw && ok) ? __ldcg(p.subk + row) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+      xv[j] = (SRC == kSrcRaw && sk[j] >= 0 && sk[j] < p.nx) ? __ldg(p.x + sk[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
       const int r = j * kTileThreads + tid;
-      const long long row = pos + r;
-      bool same = row < p.n;
-      double w = 0.0;
-      if (same) {
+      bool same = pos + r < p.n;
 #pragma unroll
-        for (int c = 0; c < NKR; ++c)
-          if (NK > 0 || c < nk) same = same && __ldcg(p.key[c] + row) == gk[c];
-        w = __ldcg(p.a + row);
-        if constexpr (SRC == kSrcRaw) {
-          const long long idx = __ldcg(p.subk + row);
-          w = (idx < 0 || idx >= p.nx) ? 0.0 : __dmul_rn(w, __ldg(p.x + idx));
-        }
-      }
-      cb[r] = w;
+      for (int c = 0; c < NKR; ++c)
+        if (NK > 0 || c < nk) same = same && kv[j][c] == gk[c];
+      cb[r] = (SRC == kSrcRaw) ? __dmul_rn(av[j], xv[j]) : av[j];
       if (!same) atomicMin(&s_end, r);
     }
     __syncthreads();

@@ -398,7 +398,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
     p.prof = prof.as<unsigned long long>();
   }
   ktimer_begin(st);
-  kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(p);
+  kern<<<(unsigned)(ntiles + 1), kTileThreads, smem, st>>>(p);  // block 0: the prefix scanner
   ktimer_end(st);
   count_launch();
   TK_CUDA(cudaGetLastError());
