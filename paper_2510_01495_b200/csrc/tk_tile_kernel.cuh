@@ -62,10 +62,7 @@ __device__ void tile_scanner(unsigned long long* status, long long ntiles) {
     int first = my_first_missing < D ? lane * D + my_first_missing : 32 * D;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    if (first == 0) {
-      __nanosleep(200);
-      continue;
-    }
+    if (first == 0) continue;  // spin: the scanner's latency is every tile's latency
     // inclusive scan of the published run [0, first)
     unsigned long long run = 0, loc[D];
 #pragma unroll
@@ -96,7 +93,7 @@ __device__ void tile_scanner(unsigned long long* status, long long ntiles) {
 __device__ __forceinline__ unsigned long long tile_wait_prefix(unsigned long long* status, long long tile,
                                                                unsigned long long agg) {
   unsigned long long s;
-  while (((s = ld_relaxed(status + tile)) >> 62) != 2) __nanosleep(128);
+  while (((s = ld_relaxed(status + tile)) >> 62) != 2) __nanosleep(32);
   return (s & kStVal) - agg;
 }
 
@@ -132,17 +129,23 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   __shared__ unsigned long long s_base;
   __shared__ int s_nlist, s_open_li, s_open_r, s_end;
   __shared__ unsigned int s_flags, s_zeros;
+  __shared__ int s_warp_heads[kTileThreads / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long ntiles = (p.n + TILE - 1) / TILE;
   if (blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
-    if (warp == 0) tile_scanner<16>(p.status, (p.n + TILE - 1) / TILE);
+    if (warp == 0) tile_scanner<8>(p.status, ntiles);
     return;
   }
+  // Blocks are dispatched in index order (the single-pass scan convention).  Block b COUNTS the
+  // heads of tile b-1 (publishing its aggregate) and FOLDS tile b-1-lag: the prefix of a tile is
+  // therefore published ~lag tiles before anyone needs it, and the fold's key columns are
+  // L2-hot from the count.
+  const long long count_tile = (long long)blockIdx.x - 1;
+  const long long fold_tile = count_tile - p.lag;
   const long long t_0 = TKT_NOW();
-  if (tid == 0) {
-    // blocks are dispatched in index order, so every predecessor tile is resident or done
-    // (the single-pass scan convention); block b handles tile b - 1
-    const long long tile = (long long)blockIdx.x - 1;
+  if (tid == 0 && fold_tile >= 0) {
+    const long long tile = fold_tile;
     s_tile = tile;
     s_nlist = 0;
     s_open_li = -1;
@@ -182,6 +185,49 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
             : "memory");
     }
   }
+
+  // ---- count the heads of tile count_tile straight from global memory, publish the aggregate ----
+  if (count_tile < ntiles) {
+    const long long cstart = count_tile * TILE;
+    const int ccnt = (int)min((long long)TILE, p.n - cstart);
+    constexpr int CJ = TILE / kTileThreads;
+    // every key load in flight at once (row and row-1: the second mostly hits L1)
+    long long cur[CJ][NKR], prv[CJ][NKR];
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) {
+      const long long row = cstart + j * kTileThreads + tid;
+      const bool ok = j * kTileThreads + tid < ccnt;
+#pragma unroll
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        cur[j][c] = ok ? p.key[c][row] : 0;
+        prv[j][c] = (ok && row > 0) ? p.key[c][row - 1] : 0;
+      }
+    }
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) {
+      const long long row = cstart + j * kTileThreads + tid;
+      bool hd = row == 0;
+#pragma unroll
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        hd = hd || cur[j][c] != prv[j][c];
+      }
+      mine += (j * kTileThreads + tid < ccnt && hd) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) s_warp_heads[warp] = mine;
+    __syncthreads();
+    if (tid == 0) {
+      int heads = 0;
+#pragma unroll
+      for (int w = 0; w < kTileThreads / 32; ++w) heads += s_warp_heads[w];
+      st_relaxed(p.status + count_tile, kStAgg | (unsigned long long)heads);
+    }
+  }
+  if (fold_tile < 0 || fold_tile >= ntiles) return;
   __syncthreads();
   const long long tile = s_tile;
   const long long start = tile * TILE;
@@ -200,28 +246,8 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     __syncthreads();
   }
 
-  // ---- w = vals * x[subk] (all gathers in flight first) and head flags ----
+  // ---- head flags first: the aggregate every later tile waits for depends only on the keys ----
   unsigned int flags = 0;
-  if constexpr (SRC == kSrcRaw) {
-    double xv[ITER], av[ITER];
-#pragma unroll
-    for (int j = 0; j < ITER; ++j) {
-      const int r = j * kTileThreads + tid;
-      xv[j] = 0.0;
-      av[j] = 0.0;
-      if (r < avail) {
-        const long long idx = s_subk[r];
-        av[j] = s_a[r];
-        if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
-        else xv[j] = __ldg(p.x + idx);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < ITER; ++j) {
-      const int r = j * kTileThreads + tid;
-      if (r < avail) s_a[r] = __dmul_rn(av[j], xv[j]);
-    }
-  }
 #pragma unroll
   for (int j = 0; j < ITER; ++j) {
     const int r = j * kTileThreads + tid;
@@ -246,13 +272,10 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     const int wi = j * (kTileThreads / 32) + warp;
     if (lane == 0 && wi < WORDS) s_head[wi] = m;
   }
-  if (flags) atomicOr(&s_flags, flags);
   __syncthreads();
   const long long t_2 = TKT_NOW();
-  if (tid == 0) TKT_ADD(1, t_2 - t_0);
-
-  if (warp == 0) {
-    // ---- popcount prefix, aggregate, decoupled look-back ----
+  int agg = 0;
+  if (warp == 0) {  // popcount prefix of the head words; publish the aggregate right away
     unsigned int w = 0;
     if (lane < TWORDS && lane * 32 < cnt) {
       w = s_head[lane];
@@ -265,20 +288,44 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
       if (lane >= o) incl += v;
     }
     if (lane < TWORDS) s_wpref[lane] = incl - __popc(w);
-    const int agg = __shfl_sync(0xffffffffu, incl, 31);
+    agg = __shfl_sync(0xffffffffu, incl, 31);  // == the aggregate the counting block published
     if (lane == 0) s_wpref[TWORDS] = agg;
-    __syncwarp();
-    named_arrive(1, kTileThreads);  // local ids ready for the classifiers
+  }
+  // ---- w = vals * x[subk] (all gathers in flight before any store) ----
+  if constexpr (SRC == kSrcRaw) {
+    double xv[ITER], av[ITER];
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int r = j * kTileThreads + tid;
+      xv[j] = 0.0;
+      av[j] = 0.0;
+      if (r < avail) {
+        const long long idx = s_subk[r];
+        av[j] = s_a[r];
+        if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+        else xv[j] = __ldg(p.x + idx);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int r = j * kTileThreads + tid;
+      if (r < avail) s_a[r] = __dmul_rn(av[j], xv[j]);
+    }
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();  // w and the local ids are ready
+  if (tid == 0) TKT_ADD(1, TKT_NOW() - t_0);
+
+  if (warp == 0) {
+    // ---- wait for this tile's exclusive prefix (the scanner block publishes it) ----
     if (lane == 0) {
-      st_relaxed(p.status + tile, kStAgg | (unsigned long long)agg);
       const unsigned long long excl = tile_wait_prefix(p.status, tile, (unsigned long long)agg);
       s_base = excl;
       if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
       TKT_ADD(2, TKT_NOW() - t_2);
     }
   } else {
-    named_bar(1, kTileThreads);
-    // ---- classify every group headed in the tile (striped over warps 1-7) ----
+    // ---- classify every group headed in the tile (striped over warps 1..) ----
     const int nheads = s_wpref[TWORDS];
     const int tc = tid - 32;
     for (int li = tc; li < nheads; li += NCLS) {

@@ -398,7 +398,9 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
     p.prof = prof.as<unsigned long long>();
   }
   ktimer_begin(st);
-  kern<<<(unsigned)(ntiles + 1), kTileThreads, smem, st>>>(p);  // block 0: the prefix scanner
+  // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
+  p.lag = std::min<long long>(1024, ntiles);
+  kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();
   TK_CUDA(cudaGetLastError());
