@@ -32,7 +32,7 @@ constexpr int tile_list_cap() {  // closed groups longer than kTileShort rows pe
 // precomputed-w sources, which have no subk column to reuse)
 template <int TILE, int HALO>
 constexpr size_t tile_smem_bytes(int ncol, int nk) {
-  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)TILE * 2 + (size_t)tile_list_cap<TILE>() * 8;
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2 + (size_t)tile_list_cap<TILE>() * 8;
 }
 
 __device__ __forceinline__ void named_arrive(int id, int threads) {
@@ -101,11 +101,10 @@ template <int SRC, int NK, int TILE, int HALO>
 __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) {
   constexpr int ROWS = TILE + HALO;
   constexpr int WORDS = ROWS / 32;
-  constexpr int TWORDS = TILE / 32;
   constexpr int ITER = (ROWS + kTileThreads - 1) / kTileThreads;
   constexpr int NKR = NK > 0 ? NK : kMaxKeep;
   constexpr int NCLS = kTileThreads - 32;  // classifier threads (warps 1-7)
-  static_assert(ROWS % 32 == 0 && TWORDS <= 32 && TILE % 32 == 0, "tile geometry");
+  static_assert(ROWS % 32 == 0 && WORDS <= 32 && TILE % 32 == 0, "tile geometry");
   const int nk = seg_nk<SRC, NK>(p);
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   // folded values by local id reuse the subk column (free once w is formed); for the
   // precomputed-w sources there is no subk column, so they get their own area
   short* s_row = reinterpret_cast<short*>(s_prev2 + 2 * nk);
-  unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_row + TILE);
+  unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_row + ROWS);
   double* s_val =
       SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : reinterpret_cast<double*>(s_list + tile_list_cap<TILE>());
 
@@ -125,7 +124,6 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   __shared__ long long s_tile;
   __shared__ int s_bulk;
   __shared__ unsigned int s_head[WORDS];
-  __shared__ int s_wpref[TWORDS + 1];
   __shared__ unsigned long long s_base;
   __shared__ int s_nlist, s_open_li, s_open_r, s_end;
   __shared__ unsigned int s_flags, s_zeros;
@@ -187,44 +185,60 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   }
 
   // ---- count the heads of tile count_tile straight from global memory, publish the aggregate ----
+  // Each warp takes 128 consecutive rows; the previous row's key comes from the neighbouring lane
+  // (lane 31 carries the row before the warp's first row, then the previous iteration's last row).
+  // The order check (kept keys non-decreasing) lives here too, while the keys are in registers.
   if (count_tile < ntiles) {
     const long long cstart = count_tile * TILE;
     const int ccnt = (int)min((long long)TILE, p.n - cstart);
     constexpr int CJ = TILE / kTileThreads;
-    // every key load in flight at once (row and row-1: the second mostly hits L1)
-    long long cur[CJ][NKR], prv[CJ][NKR];
+    const int wrow0 = warp * (TILE / (kTileThreads / 32));
+    long long cur[CJ][NKR], edge[NKR];
 #pragma unroll
-    for (int j = 0; j < CJ; ++j) {
-      const long long row = cstart + j * kTileThreads + tid;
-      const bool ok = j * kTileThreads + tid < ccnt;
-#pragma unroll
-      for (int c = 0; c < NKR; ++c) {
-        if (NK == 0 && c >= nk) break;
-        cur[j][c] = ok ? p.key[c][row] : 0;
-        prv[j][c] = (ok && row > 0) ? p.key[c][row - 1] : 0;
-      }
-    }
-    int mine = 0;
-#pragma unroll
-    for (int j = 0; j < CJ; ++j) {
-      const long long row = cstart + j * kTileThreads + tid;
-      bool hd = row == 0;
+    for (int j = 0; j < CJ; ++j) {  // every key load in flight at once
+      const int rl = wrow0 + j * 32 + lane;
+      const bool ok = rl < ccnt;
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
-        hd = hd || cur[j][c] != prv[j][c];
+        cur[j][c] = ok ? p.key[c][cstart + rl] : 0;
       }
-      mine += (j * kTileThreads + tid < ccnt && hd) ? 1 : 0;
     }
+    {
+      const bool ok = lane == 31 && wrow0 < ccnt && cstart + wrow0 > 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if (lane == 0) s_warp_heads[warp] = mine;
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        edge[c] = ok ? p.key[c][cstart + wrow0 - 1] : 0;
+      }
+    }
+    int heads = 0;
+    bool unsorted = false;
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) {
+      const int rl = wrow0 + j * 32 + lane;
+      bool eq = true, less = false;
+#pragma unroll
+      for (int c = 0; c < NKR; ++c) {
+        if (NK == 0 && c >= nk) break;
+        const long long give = lane == 31 ? (j ? cur[j - 1][c] : edge[c]) : cur[j][c];
+        const long long pv = __shfl_sync(0xffffffffu, give, (lane + 31) & 31);
+        less = less || (eq && cur[j][c] < pv);
+        eq = eq && cur[j][c] == pv;
+      }
+      const bool first = cstart + rl == 0;
+      const bool ok = rl < ccnt;
+      unsorted = unsorted || (ok && less && !first);
+      heads += __popc(__ballot_sync(0xffffffffu, ok && (!eq || first)));
+    }
+    if (unsorted) atomicOr(&p.ctr->flags, kFlagUnsorted);  // rare: the host takes the sort path
+    if (lane == 0) s_warp_heads[warp] = heads;
     __syncthreads();
     if (tid == 0) {
-      int heads = 0;
+      int h = 0;
 #pragma unroll
-      for (int w = 0; w < kTileThreads / 32; ++w) heads += s_warp_heads[w];
-      st_relaxed(p.status + count_tile, kStAgg | (unsigned long long)heads);
+      for (int w = 0; w < kTileThreads / 32; ++w) h += s_warp_heads[w];
+      st_relaxed(p.status + count_tile, kStAgg | (unsigned long long)h);
     }
   }
   if (fold_tile < 0 || fold_tile >= ntiles) return;
@@ -246,51 +260,52 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     __syncthreads();
   }
 
-  // ---- head flags first: the aggregate every later tile waits for depends only on the keys ----
-  unsigned int flags = 0;
+  // ---- head bitmask of the stage (key equality with the previous row) ----
+  unsigned int hmask[ITER];
 #pragma unroll
   for (int j = 0; j < ITER; ++j) {
     const int r = j * kTileThreads + tid;
     bool hd = false;
     if (r < avail) {
-      int cmp = 0;
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
         const long long va = s_key[c * ROWS + r];
         const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
-        if (va != vb) {
-          cmp = va < vb ? -1 : 1;
-          break;
-        }
+        hd = hd || va != vb;
       }
-      if (r == 0 && start == 0) cmp = 1;
-      hd = cmp != 0;
-      if (cmp < 0 && r < cnt) flags |= kFlagUnsorted;
+      if (r == 0 && start == 0) hd = true;
     }
-    const unsigned int m = __ballot_sync(0xffffffffu, hd);
+    hmask[j] = __ballot_sync(0xffffffffu, hd);
     const int wi = j * (kTileThreads / 32) + warp;
-    if (lane == 0 && wi < WORDS) s_head[wi] = m;
+    if (lane == 0 && wi < WORDS) s_head[wi] = hmask[j];
   }
   __syncthreads();
   const long long t_2 = TKT_NOW();
-  int agg = 0;
-  if (warp == 0) {  // popcount prefix of the head words; publish the aggregate right away
-    unsigned int w = 0;
-    if (lane < TWORDS && lane * 32 < cnt) {
-      w = s_head[lane];
-      if (lane * 32 + 32 > cnt) w &= (1u << (cnt - lane * 32)) - 1u;
-    }
-    int incl = __popc(w);
+  // ---- every warp: popcount prefix of the head words (redundant per warp: no extra barrier);
+  //      each head row records itself at its local id ----
+  int agg, ptot;
+  {
+    const unsigned int hw = lane < WORDS ? s_head[lane] : 0u;
+    int incl = __popc(hw);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    if (lane < TWORDS) s_wpref[lane] = incl - __popc(w);
-    agg = __shfl_sync(0xffffffffu, incl, 31);  // == the aggregate the counting block published
-    if (lane == 0) s_wpref[TWORDS] = agg;
+    const int excl = incl - __popc(hw);
+    ptot = __shfl_sync(0xffffffffu, incl, 31);  // heads in the stage (tile + halo)
+    // heads in the tile proper == the aggregate the counting block published
+    agg = __shfl_sync(0xffffffffu, excl + __popc(hw & ((1u << (cnt & 31)) - 1u)), cnt >> 5);
+    const unsigned int lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int wi = j * (kTileThreads / 32) + warp;
+      const int wex = __shfl_sync(0xffffffffu, excl, wi & 31);
+      if ((hmask[j] >> lane) & 1u) s_row[wex + __popc(hmask[j] & lt)] = (short)(j * kTileThreads + tid);
+    }
   }
+  unsigned int flags = 0;
   // ---- w = vals * x[subk] (all gathers in flight before any store) ----
   if constexpr (SRC == kSrcRaw) {
     double xv[ITER], av[ITER];
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
       if (r < avail) {
         const long long idx = s_subk[r];
         av[j] = s_a[r];
-        if (idx < 0 || idx >= p.nx) flags |= kFlagIndex;
+        if ((unsigned long long)idx >= (unsigned long long)p.nx) flags |= kFlagIndex;
         else xv[j] = __ldg(p.x + idx);
       }
     }
@@ -313,7 +328,7 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     }
   }
   if (flags) atomicOr(&s_flags, flags);
-  __syncthreads();  // w and the local ids are ready
+  __syncthreads();  // w and the head rows are ready
   if (tid == 0) TKT_ADD(1, TKT_NOW() - t_0);
 
   if (warp == 0) {
@@ -326,34 +341,17 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     }
   } else {
     // ---- classify every group headed in the tile (striped over warps 1..) ----
-    const int nheads = s_wpref[TWORDS];
     const int tc = tid - 32;
-    for (int li = tc; li < nheads; li += NCLS) {
-      int lo = 0, hi = TWORDS - 1;  // word holding the li-th head
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_wpref[mid] <= li) lo = mid;
-        else hi = mid - 1;
-      }
-      const int r = lo * 32 + (int)__fns(s_head[lo], 0, li - s_wpref[lo] + 1);
-      int end = avail;
-      {
-        const int q1 = r + 1;
-        int wi = q1 >> 5;
-        unsigned int wb = (q1 < avail) ? (s_head[wi] & (0xffffffffu << (q1 & 31))) : 0u;
-        while (wb == 0 && (wi + 1) * 32 < avail) wb = s_head[++wi];
-        if (wb) end = min(avail, wi * 32 + __ffs(wb) - 1);
-      }
-      const bool open = end == avail && start + avail < p.n;
-      if (open) {
+    for (int li = tc; li < agg; li += NCLS) {
+      const int r = s_row[li];
+      const bool last = li + 1 >= ptot;  // no later head in the stage
+      const int end = last ? avail : s_row[li + 1];
+      if (last && start + avail < p.n) {
         s_open_li = li;
         s_open_r = r;
-        s_row[li] = -1;
       } else if (end - r <= kTileShort) {
         s_val[li] = fold_run(s_a, r + 1, end, s_a[r]);
-        s_row[li] = (short)r;
       } else {
-        s_row[li] = (short)r;
         const int q = atomicAdd(&s_nlist, 1);
         s_list[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
       }
@@ -373,11 +371,11 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
 
   // ---- coalesced output of every group closed inside the stage ----
   const long long base = (long long)s_base;
-  const int nheads = s_wpref[TWORDS];
+  const int open_li = s_open_li;
   unsigned int zeros = 0;
-  for (int li = tid; li < nheads; li += kTileThreads) {
+  for (int li = tid; li < agg; li += kTileThreads) {
+    if (li == open_li) continue;
     const int r = s_row[li];
-    if (r < 0) continue;
     const double v = s_val[li];
     const long long g = base + li;
     p.out_vals[g] = v;
@@ -399,7 +397,6 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     }
   }
   if (zeros) atomicAdd(&s_zeros, zeros);
-  const int open_li = s_open_li;
   if (tid == 0) {
     TKT_ADD(4, TKT_NOW() - t_3);
     TKT_ADD(6, 1);
