@@ -20,7 +20,16 @@
 
 namespace tk {
 
-constexpr int kTileThreads = 128;  // threads per CTA (8 CTAs per SM)
+#ifndef TK_TILE_MINB
+#define TK_TILE_MINB 8  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef TK_TILE_PF
+#define TK_TILE_PF 256  // tiles ahead of the count whose columns are prefetched into L2
+#endif
+#ifndef TK_SCAN_D
+#define TK_SCAN_D 8  // status words per scanner lane per round
+#endif
+constexpr int kTileThreads = 128;  // threads per CTA
 constexpr int kTileShort = 8;  // folded inline by the classifying thread
 
 template <int TILE>
@@ -98,12 +107,11 @@ __device__ __forceinline__ unsigned long long tile_wait_prefix(unsigned long lon
 }
 
 template <int SRC, int NK, int TILE, int HALO>
-__global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) {
+__global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(SegParams p) {
   constexpr int ROWS = TILE + HALO;
   constexpr int WORDS = ROWS / 32;
   constexpr int ITER = (ROWS + kTileThreads - 1) / kTileThreads;
   constexpr int NKR = NK > 0 ? NK : kMaxKeep;
-  constexpr int NCLS = kTileThreads - 32;  // classifier threads (warps 1-7)
   static_assert(ROWS % 32 == 0 && WORDS <= 32 && TILE % 32 == 0, "tile geometry");
   const int nk = seg_nk<SRC, NK>(p);
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
@@ -125,14 +133,14 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
   __shared__ int s_bulk;
   __shared__ unsigned int s_head[WORDS];
   __shared__ unsigned long long s_base;
-  __shared__ int s_nlist, s_open_li, s_open_r, s_end;
-  __shared__ unsigned int s_flags, s_zeros;
+  __shared__ int s_nlist, s_open_li, s_open_r;
+  __shared__ unsigned int s_flags;
   __shared__ int s_warp_heads[kTileThreads / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long ntiles = (p.n + TILE - 1) / TILE;
   if (blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
-    if (warp == 0) tile_scanner<8>(p.status, ntiles);
+    if (warp == 0) tile_scanner<TK_SCAN_D>(p.status, ntiles);
     return;
   }
   // Blocks are dispatched in index order (the single-pass scan convention).  Block b COUNTS the
@@ -148,7 +156,6 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     s_nlist = 0;
     s_open_li = -1;
     s_flags = 0;
-    s_zeros = 0;
     const long long start = tile * TILE;
     const long long avail = min((long long)ROWS, p.n - start);
     const bool bulk = p.bulk_ok && avail == ROWS;
@@ -181,6 +188,21 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
                 smem_u32(s_subk)),
             "l"(p.subk + start), "r"(bytes), "r"(smem_u32(&s_bar))
             : "memory");
+    }
+  }
+
+  // ---- L2 prefetch of every column of tile count_tile + TK_TILE_PF: the count loads of that tile
+  //      and, ~lag tiles later, its fold's TMA then hit L2; HBM sees only these async requests ----
+  if (TK_TILE_PF > 0 && warp == 1 && lane < ncol) {
+    const long long pt = count_tile + TK_TILE_PF;
+    if (pt < ntiles) {
+      const long long ps = pt * TILE;
+      const uint32_t bytes = (uint32_t)(min((long long)TILE, p.n - ps) * 8) & ~15u;
+      const void* src = lane < nk ? (const void*)(p.key[lane] + ps)
+                        : lane == nk ? (const void*)(p.a + ps)
+                                     : (const void*)(p.subk + ps);
+      if (bytes)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
     }
   }
 
@@ -305,6 +327,13 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
       if ((hmask[j] >> lane) & 1u) s_row[wex + __popc(hmask[j] & lt)] = (short)(j * kTileThreads + tid);
     }
   }
+  if (warp == 0 && lane == 0) {
+    // ---- this tile's exclusive prefix (the scanner block published it ~lag tiles ago) ----
+    const unsigned long long excl = tile_wait_prefix(p.status, tile, (unsigned long long)agg);
+    s_base = excl;
+    if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
+    TKT_ADD(2, TKT_NOW() - t_2);
+  }
   unsigned int flags = 0;
   // ---- w = vals * x[subk] (all gathers in flight before any store) ----
   if constexpr (SRC == kSrcRaw) {
@@ -328,58 +357,16 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
     }
   }
   if (flags) atomicOr(&s_flags, flags);
-  __syncthreads();  // w and the head rows are ready
-  if (tid == 0) TKT_ADD(1, TKT_NOW() - t_0);
-
-  if (warp == 0) {
-    // ---- wait for this tile's exclusive prefix (the scanner block publishes it) ----
-    if (lane == 0) {
-      const unsigned long long excl = tile_wait_prefix(p.status, tile, (unsigned long long)agg);
-      s_base = excl;
-      if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
-      TKT_ADD(2, TKT_NOW() - t_2);
-    }
-  } else {
-    // ---- classify every group headed in the tile (striped over warps 1..) ----
-    const int tc = tid - 32;
-    for (int li = tc; li < agg; li += NCLS) {
-      const int r = s_row[li];
-      const bool last = li + 1 >= ptot;  // no later head in the stage
-      const int end = last ? avail : s_row[li + 1];
-      if (last && start + avail < p.n) {
-        s_open_li = li;
-        s_open_r = r;
-      } else if (end - r <= kTileShort) {
-        s_val[li] = fold_run(s_a, r + 1, end, s_a[r]);
-      } else {
-        const int q = atomicAdd(&s_nlist, 1);
-        s_list[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
-      }
-    }
-    named_bar(2, NCLS);
-    // ---- longer closed groups: one per thread, packed into the first warps ----
-    const int nl = s_nlist;
-    for (int q = tc; q < nl; q += NCLS) {
-      const unsigned long long e = s_list[q];
-      const int li = (int)(e & 0xffff), r = (int)((e >> 16) & 0xffff), end = (int)(e >> 32);
-      s_val[li] = fold_run(s_a, r + 1, end, s_a[r]);
-    }
+  __syncthreads();  // w, the head rows and the base are ready
+  if (tid == 0) {
+    if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+    TKT_ADD(1, TKT_NOW() - t_0);
   }
-  __syncthreads();
-  const long long t_3 = TKT_NOW();
-  if (tid == 0) TKT_ADD(3, t_3 - t_2);
-
-  // ---- coalesced output of every group closed inside the stage ----
   const long long base = (long long)s_base;
-  const int open_li = s_open_li;
-  unsigned int zeros = 0;
-  for (int li = tid; li < agg; li += kTileThreads) {
-    if (li == open_li) continue;
-    const int r = s_row[li];
-    const double v = s_val[li];
+  // one group's output row: (kept key of its head row, folded value) at base + local id
+  auto emit = [&](int li, int r, double v) {
     const long long g = base + li;
     p.out_vals[g] = v;
-    zeros += v == 0.0;
     if constexpr (SRC == kSrcLinKey) {
       long long lin = s_key[r];
       long long* o = p.out_subs + g * p.out_nk;
@@ -395,44 +382,69 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
         p.out_subs[g * p.out_nk + c] = s_key[c * ROWS + r];
       }
     }
+  };
+
+  // ---- classify every group headed in the tile (striped: consecutive lanes write consecutive
+  //      output rows); short groups are folded and written at once ----
+  unsigned int zeros = 0;
+  for (int li = tid; li < agg; li += kTileThreads) {
+    const int r = s_row[li];
+    const bool last = li + 1 >= ptot;  // no later head in the stage
+    const int end = last ? avail : s_row[li + 1];
+    if (last && start + avail < p.n) {
+      s_open_li = li;
+      s_open_r = r;
+    } else if (end - r <= kTileShort) {
+      const double v = fold_run(s_a, r + 1, end, s_a[r]);
+      emit(li, r, v);
+      zeros += v == 0.0;
+    } else {
+      const int q = atomicAdd(&s_nlist, 1);
+      s_list[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
+    }
   }
-  if (zeros) atomicAdd(&s_zeros, zeros);
+  __syncthreads();  // the long-group list and the open group are known
+  const long long t_3 = TKT_NOW();
+  if (tid == 0) TKT_ADD(3, t_3 - t_2);
+  // ---- longer closed groups: one per thread, packed into the first warps; a warp with nothing
+  //      left exits here, so the SM can start another tile while the folds run ----
+  const int nl = s_nlist;
+  const int open_li = s_open_li;
+  for (int q = tid; q < nl; q += kTileThreads) {
+    const unsigned long long e = s_list[q];
+    const int li = (int)(e & 0xffff), r = (int)((e >> 16) & 0xffff), end = (int)(e >> 32);
+    const double v = fold_run(s_a, r + 1, end, s_a[r]);
+    emit(li, r, v);
+    zeros += v == 0.0;
+  }
+  zeros = __reduce_add_sync(0xffffffffu, zeros);
+  if (lane == 0 && zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
   if (tid == 0) {
     TKT_ADD(4, TKT_NOW() - t_3);
     TKT_ADD(6, 1);
+    if (open_li < 0) TKT_ADD(9, TKT_NOW() - t_0);
   }
-  if (open_li < 0) {
-    __syncthreads();
-    if (tid == 0) {
-      if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
-      if (s_flags) atomicOr(&p.ctr->flags, s_flags);
-      TKT_ADD(9, TKT_NOW() - t_0);
-    }
-    return;
-  }
+  if (warp != 0 || open_li < 0) return;
   const long long t_4 = TKT_NOW();
 
-  // ---- the group that runs past the halo: stream its rows in 1024-row chunks (L2-hot: the next
-  //      tiles' CTAs are reading them), thread 0 folds from smem ----
+  // ---- the group that runs past the halo, finished by warp 0 alone: 128-row chunks (L2-hot: the
+  //      next tiles' CTAs read them), w staged in the free subk column; the next chunk's loads are
+  //      in flight while lane 0 folds the current one ----
   const int r0 = s_open_r;
   long long gk[NKR];
 #pragma unroll
   for (int c = 0; c < NKR; ++c)
     if (NK > 0 || c < nk) gk[c] = s_key[c * ROWS + r0];
-  double acc = 0.0;  // meaningful in thread 0, which does every fold of this group
-  if (tid == 0) acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
-  __syncthreads();  // the stage is free from here on: reuse it as the chunk buffer
-  double* cb = reinterpret_cast<double*>(st);
-  constexpr int CH = 4 * kTileThreads;
-  for (long long pos = start + avail; pos < p.n; pos += CH) {
-    if (tid == 0) s_end = CH;
-    __syncthreads();
-    constexpr int RPT = CH / kTileThreads;
-    long long kv[RPT][NKR], sk[RPT];
-    double av[RPT], xv[RPT];
+  double acc = 0.0;  // meaningful in lane 0, which does every fold of this group
+  if (lane == 0) acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
+  double* cb = SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : s_val;
+  constexpr int RW = 4, CH = 32 * RW;
+  long long kv[RW][NKR], sk[RW];
+  double av[RW];
+  auto load_chunk = [&](long long pos) {
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {  // every load of the chunk in flight at once
-      const long long row = pos + j * kTileThreads + tid;
+    for (int j = 0; j < RW; ++j) {  // every load of the chunk in flight at once
+      const long long row = pos + j * 32 + lane;
       const bool ok = row < p.n;
 #pragma unroll
       for (int c = 0; c < NKR; ++c)
@@ -440,34 +452,39 @@ __global__ void __launch_bounds__(kTileThreads, 8) ttv_tile_kernel(SegParams p) 
       av[j] = ok ? __ldcg(p.a + row) : 0.0;
       sk[j] = (SRC == kSrcRaw && ok) ? __ldcg(p.subk + row) : 0;
     }
+  };
+  long long pos = start + avail;
+  load_chunk(pos);
+  while (true) {
+    int end = CH;
 #pragma unroll
-    for (int j = 0; j < RPT; ++j)
-      xv[j] = (SRC == kSrcRaw && sk[j] >= 0 && sk[j] < p.nx) ? __ldg(p.x + sk[j]) : 0.0;
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int r = j * kTileThreads + tid;
+    for (int j = 0; j < RW; ++j) {
+      const int r = j * 32 + lane;
       bool same = pos + r < p.n;
 #pragma unroll
       for (int c = 0; c < NKR; ++c)
         if (NK > 0 || c < nk) same = same && kv[j][c] == gk[c];
-      cb[r] = (SRC == kSrcRaw) ? __dmul_rn(av[j], xv[j]) : av[j];
-      if (!same) atomicMin(&s_end, r);
+      double w = av[j];
+      if constexpr (SRC == kSrcRaw)
+        w = __dmul_rn(w, (unsigned long long)sk[j] < (unsigned long long)p.nx ? __ldg(p.x + sk[j]) : 0.0);
+      cb[r] = w;
+      const unsigned int m = __ballot_sync(0xffffffffu, !same);
+      if (end == CH && m) end = j * 32 + __ffs(m) - 1;
     }
-    __syncthreads();
-    const int end = s_end;
-    if (tid == 0) acc = fold_run(cb, 0, end, acc);
-    if (end < CH) break;
-    __syncthreads();
+    __syncwarp();
+    const bool more = end == CH && pos + CH < p.n;
+    if (more) load_chunk(pos + CH);  // in flight during the fold below
+    if (lane == 0) acc = fold_run(cb, 0, end, acc);
+    __syncwarp();
+    if (!more) break;
+    pos += CH;
   }
-  if (tid == 0) {
-    const long long g = base + open_li;
-    long long kv[NKR];
+  if (lane == 0) {
+    long long k[NKR];
 #pragma unroll
     for (int c = 0; c < NKR; ++c)
-      if (NK > 0 || c < nk) kv[c] = gk[c];
-    seg_emit<SRC>(p, g, kv, acc);
-    if (s_zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)s_zeros);
-    if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+      if (NK > 0 || c < nk) k[c] = gk[c];
+    seg_emit<SRC>(p, base + open_li, k, acc);
     const long long t_5 = TKT_NOW();
     TKT_ADD(5, t_5 - t_4);
     TKT_ADD(7, 1);
