@@ -20,7 +20,9 @@ enum : unsigned int {
   kFlagIndex = 1u,     // contracted-mode index outside x -> DimensionError
   kFlagUnsorted = 2u,  // kept-mode keys not non-decreasing -> take the sort path
   kFlagKeptOob = 4u,   // kept-mode index outside its dimension (garbage input)
+  kFlagStall = 8u,     // a cross-CTA wait gave up (watchdog): the call fails instead of hanging
 };
+constexpr unsigned int kSpinLimit = 1u << 25;  // polls (>= ~64 ns each) before a wait gives up
 
 // Per-call scalars written by the kernels and read back by the host once.
 struct Counters {

@@ -152,6 +152,9 @@ __device__ __forceinline__ bool key_eq_global(const SegParams& p, int nk, long l
 
 // acc, then s_a[j .. end) added in order (independent loads, dependent adds).
 __device__ __forceinline__ double fold_run(const double* s_a, int j, int end, double acc) {
+#ifdef TK_DIAG_NOFOLD  // diagnostics only: wrong values, measures the cost of the serial folds
+  return acc + (end > j ? s_a[end - 1] : 0.0);
+#endif
   for (; j + 4 <= end; j += 4) {
     const double v0 = s_a[j], v1 = s_a[j + 1], v2 = s_a[j + 2], v3 = s_a[j + 3];
     acc = __dadd_rn(acc, v0);

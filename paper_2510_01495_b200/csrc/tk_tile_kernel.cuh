@@ -29,7 +29,31 @@ namespace tk {
 #ifndef TK_SCAN_D
 #define TK_SCAN_D 8  // status words per scanner lane per round
 #endif
-constexpr int kTileThreads = 128;  // threads per CTA
+#ifndef TK_TILE_THREADS
+#define TK_TILE_THREADS 128
+#endif
+constexpr int kTileThreads = TK_TILE_THREADS;  // threads per CTA
+// Development trace (-DTK_TRACE): per block, clock64 at the phase boundaries into p.prof[block*8 + slot]
+// (slot 0 = smid << 48 | start clock); the host dumps it to $TK_TRACE_FILE.
+#ifdef TK_TRACE
+#define TKR_START()                                                                                    \
+  if (threadIdx.x == 0 && p.prof) {                                                                    \
+    unsigned int smid_;                                                                                \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                                \
+    p.prof[(size_t)blockIdx.x * 8] = ((unsigned long long)smid_ << 48) | (clock64() & ((1ull << 48) - 1)); \
+  }
+#define TKR(slot) \
+  if (p.prof) p.prof[(size_t)blockIdx.x * 8 + (slot)] = clock64() & ((1ull << 48) - 1)
+#else
+#define TKR_START()
+#define TKR(slot)
+#endif
+constexpr int kTileWarps = kTileThreads / 32;
+// Tile status word: while counting, every warp adds (1 << 56) | its head count (so the aggregate is
+// complete when the warp field reads kTileWarps); the scanner then stores kStPre | inclusive prefix.
+constexpr int kStWarpShift = 56;
+constexpr unsigned long long kStCntMask = (1ull << kStWarpShift) - 1;
+constexpr unsigned long long kStReady = (unsigned long long)kTileWarps << kStWarpShift;
 constexpr int kTileShort = 8;  // folded inline by the classifying thread
 
 template <int TILE>
@@ -44,6 +68,11 @@ constexpr size_t tile_smem_bytes(int ncol, int nk) {
   return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2 + (size_t)tile_list_cap<TILE>() * 8;
 }
 
+template <int SRC, int TILE, int HALO>
+constexpr size_t tile_total_smem(int ncol, int nk) {
+  return tile_smem_bytes<TILE, HALO>(ncol, nk) + (SRC == kSrcRaw ? 0 : (size_t)TILE * 8);
+}
+
 __device__ __forceinline__ void named_arrive(int id, int threads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -53,31 +82,49 @@ __device__ __forceinline__ void named_arrive(int id, int threads) {
 // already-published aggregates in the next 32*D tiles (one L2 round trip), scans it, publishes the
 // prefixes and advances.  A tile therefore waits ~one round trip after its own aggregate, and
 // polls only its own status word -- no wide look-back windows hammering L2.
+// A wait that gives up records where (Counters::q_head = site << 56 | tile) and raises kFlagStall.
+__device__ __forceinline__ void tile_stall(Counters* ctr, unsigned long long site, long long tile) {
+  atomicOr(&ctr->flags, kFlagStall);
+  atomicExch(&ctr->q_head, (site << 56) | (unsigned long long)tile);
+}
+
 template <int D>
-__device__ void tile_scanner(unsigned long long* status, long long ntiles) {
+__device__ void tile_scanner(unsigned long long* status, long long ntiles, Counters* ctr) {
   const int lane = threadIdx.x & 31;
   unsigned long long carry = 0;
   long long w = 0;
+  unsigned int spins = 0;
   while (w < ntiles) {
     unsigned long long v[D];
     int my_first_missing = D;  // first unpublished element of this lane
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       const long long t = w + lane * D + i;
-      v[i] = t < ntiles ? ld_relaxed(status + t) : (kStAgg | 0ull);
-      if ((v[i] >> 62) == 0 && my_first_missing == D) my_first_missing = i;
+      v[i] = t < ntiles ? ld_relaxed(status + t) : kStReady;
+      if ((v[i] >> kStWarpShift) != (unsigned long long)kTileWarps && my_first_missing == D) my_first_missing = i;
     }
     // global position of the first unpublished tile in the window
     int first = my_first_missing < D ? lane * D + my_first_missing : 32 * D;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    if (first == 0) continue;  // spin: the scanner's latency is every tile's latency
+    if (first == 0) {  // spin: the scanner's latency is every tile's latency
+#ifdef TK_NO_WATCHDOG
+      if (false) {
+#else
+      if (++spins == kSpinLimit) {
+#endif
+        if (lane == 0) tile_stall(ctr, 1, w);
+        return;
+      }
+      continue;
+    }
+    spins = 0;
     // inclusive scan of the published run [0, first)
     unsigned long long run = 0, loc[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       const int e = lane * D + i;
-      run += (e < first) ? (v[i] & kStVal) : 0ull;
+      run += (e < first) ? (v[i] & kStCntMask) : 0ull;
       loc[i] = run;
     }
     unsigned long long incl = run;
@@ -99,11 +146,20 @@ __device__ void tile_scanner(unsigned long long* status, long long ntiles) {
 }
 
 // A tile's exclusive prefix once the scanner has published it (tile 0: 0).
-__device__ __forceinline__ unsigned long long tile_wait_prefix(unsigned long long* status, long long tile,
-                                                               unsigned long long agg) {
-  unsigned long long s;
-  while (((s = ld_relaxed(status + tile)) >> 62) != 2) __nanosleep(32);
-  return (s & kStVal) - agg;
+// (false: the watchdog gave up)
+// `s` is an early read of the status word (issued at block start, usually already the prefix).
+__device__ __forceinline__ bool tile_wait_prefix(unsigned long long* status, long long tile, unsigned long long agg,
+                                                 unsigned long long s, unsigned long long* excl) {
+  unsigned int spins = 0;
+  while ((s >> 62) != 2) {
+#ifndef TK_NO_WATCHDOG
+    if (++spins == kSpinLimit) return false;
+#endif
+    __nanosleep(32);
+    s = ld_relaxed(status + tile);
+  }
+  *excl = (s & kStVal) - agg;
+  return true;
 }
 
 template <int SRC, int NK, int TILE, int HALO>
@@ -135,12 +191,11 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   __shared__ unsigned long long s_base;
   __shared__ int s_nlist, s_open_li, s_open_r;
   __shared__ unsigned int s_flags;
-  __shared__ int s_warp_heads[kTileThreads / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long ntiles = (p.n + TILE - 1) / TILE;
   if (blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
-    if (warp == 0) tile_scanner<TK_SCAN_D>(p.status, ntiles);
+    if (warp == 0) tile_scanner<TK_SCAN_D>(p.status, ntiles, p.ctr);
     return;
   }
   // Blocks are dispatched in index order (the single-pass scan convention).  Block b COUNTS the
@@ -149,7 +204,11 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // L2-hot from the count.
   const long long count_tile = (long long)blockIdx.x - 1;
   const long long fold_tile = count_tile - p.lag;
-  const long long t_0 = TKT_NOW();
+  TKR_START();
+  // the fold tile's status word, read now: published ~lag tiles ago, so this is almost always the
+  // prefix already and its L2 round trip overlaps the count instead of delaying the fold
+  unsigned long long pre = 0;
+  if (tid == 0 && fold_tile >= 0 && fold_tile < ntiles) pre = ld_relaxed(p.status + fold_tile);
   if (tid == 0 && fold_tile >= 0) {
     const long long tile = fold_tile;
     s_tile = tile;
@@ -191,6 +250,8 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   }
 
+  __syncthreads();  // the mbarrier is initialised and the tile's copies are issued
+
   // ---- L2 prefetch of every column of tile count_tile + TK_TILE_PF: the count loads of that tile
   //      and, ~lag tiles later, its fold's TMA then hit L2; HBM sees only these async requests ----
   if (TK_TILE_PF > 0 && warp == 1 && lane < ncol) {
@@ -210,11 +271,45 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // Each warp takes 128 consecutive rows; the previous row's key comes from the neighbouring lane
   // (lane 31 carries the row before the warp's first row, then the previous iteration's last row).
   // The order check (kept keys non-decreasing) lives here too, while the keys are in registers.
+#ifdef TK_LAG0  // the fold publishes its own aggregate: no separate count
+  if (false) {
+#else
   if (count_tile < ntiles) {
+#endif
     const long long cstart = count_tile * TILE;
     const int ccnt = (int)min((long long)TILE, p.n - cstart);
+    const int wrow0 = warp * (TILE / kTileWarps);
+    int heads = 0;
+    constexpr int WROWS = TILE / kTileWarps;
+    if (NK > 0 && WROWS % 64 == 0 && ccnt == TILE && p.bulk_ok) {
+      // Full tile, 16-byte aligned columns: 16-byte loads of row pairs (2*lane, 2*lane+1) per
+      // 64-row block; only the pair's first row needs a neighbour (lane-1's second row).
+      constexpr int NB = WROWS / 64 > 0 ? WROWS / 64 : 1;
+      constexpr int NKV = NK > 0 ? NK : 1;
+      longlong2 v[NB][NKV];
+      long long edge[NKV];
+      const long long r0 = cstart + wrow0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NKV; ++c) v[b][c] = reinterpret_cast<const longlong2*>(p.key[c] + r0 + 64 * b)[lane];
+#pragma unroll
+      for (int c = 0; c < NKV; ++c) edge[c] = (lane == 31 && r0 > 0) ? p.key[c][r0 - 1] : 0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        bool ne0 = false, ne1 = false;
+#pragma unroll
+        for (int c = 0; c < NKV; ++c) {
+          const long long give = lane == 31 ? (b ? v[b - 1][c].y : edge[c]) : v[b][c].y;
+          const long long pv = __shfl_sync(0xffffffffu, give, (lane + 31) & 31);  // every lane
+          ne0 = ne0 || v[b][c].x != pv;
+          ne1 = ne1 || v[b][c].y != v[b][c].x;
+        }
+        heads += (ne0 || r0 + 64 * b + 2 * lane == 0) + ne1;
+      }
+      heads = __reduce_add_sync(0xffffffffu, heads);
+    } else {
     constexpr int CJ = TILE / kTileThreads;
-    const int wrow0 = warp * (TILE / (kTileThreads / 32));
     long long cur[CJ][NKR], edge[NKR];
 #pragma unroll
     for (int j = 0; j < CJ; ++j) {  // every key load in flight at once
@@ -234,44 +329,31 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
         edge[c] = ok ? p.key[c][cstart + wrow0 - 1] : 0;
       }
     }
-    int heads = 0;
-    bool unsorted = false;
 #pragma unroll
     for (int j = 0; j < CJ; ++j) {
       const int rl = wrow0 + j * 32 + lane;
-      bool eq = true, less = false;
+      bool ne = false;
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
         const long long give = lane == 31 ? (j ? cur[j - 1][c] : edge[c]) : cur[j][c];
-        const long long pv = __shfl_sync(0xffffffffu, give, (lane + 31) & 31);
-        less = less || (eq && cur[j][c] < pv);
-        eq = eq && cur[j][c] == pv;
+        const long long pv = __shfl_sync(0xffffffffu, give, (lane + 31) & 31);  // every lane
+        ne = ne || cur[j][c] != pv;
       }
-      const bool first = cstart + rl == 0;
-      const bool ok = rl < ccnt;
-      unsorted = unsorted || (ok && less && !first);
-      heads += __popc(__ballot_sync(0xffffffffu, ok && (!eq || first)));
+      heads += __popc(__ballot_sync(0xffffffffu, rl < ccnt && (ne || cstart + rl == 0)));
     }
-    if (unsorted) atomicOr(&p.ctr->flags, kFlagUnsorted);  // rare: the host takes the sort path
-    if (lane == 0) s_warp_heads[warp] = heads;
-    __syncthreads();
-    if (tid == 0) {
-      int h = 0;
-#pragma unroll
-      for (int w = 0; w < kTileThreads / 32; ++w) h += s_warp_heads[w];
-      st_relaxed(p.status + count_tile, kStAgg | (unsigned long long)h);
     }
+    if (lane == 0) atomicAdd(p.status + count_tile, (1ull << kStWarpShift) | (unsigned long long)heads);
+    if (tid == 0) TKR(1);
   }
   if (fold_tile < 0 || fold_tile >= ntiles) return;
-  __syncthreads();
   const long long tile = s_tile;
   const long long start = tile * TILE;
   const int cnt = (int)min((long long)TILE, p.n - start);
   const int avail = (int)min((long long)ROWS, p.n - start);
   if (s_bulk) {
     mbar_wait(&s_bar, 0);
-    if (tid == 0) TKT_ADD(0, TKT_NOW() - t_0);
+    if (tid == 0) TKR(2);
   } else {
     for (int r = tid; r < avail; r += kTileThreads) {
       for (int c = 0; c < nk; ++c) s_key[(size_t)c * ROWS + r] = p.key[c][start + r];
@@ -282,28 +364,32 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     __syncthreads();
   }
 
-  // ---- head bitmask of the stage (key equality with the previous row) ----
+  // ---- head bitmask of the stage (key equality with the previous row) and the order check
+  //      (kept keys must be non-decreasing: lexicographic compare, same loads) ----
   unsigned int hmask[ITER];
+  bool unsorted = false;
 #pragma unroll
   for (int j = 0; j < ITER; ++j) {
     const int r = j * kTileThreads + tid;
     bool hd = false;
     if (r < avail) {
+      bool less = false;
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
         const long long va = s_key[c * ROWS + r];
         const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
+        less = less || (!hd && va < vb);
         hd = hd || va != vb;
       }
       if (r == 0 && start == 0) hd = true;
+      else unsorted = unsorted || (less && r < cnt);
     }
     hmask[j] = __ballot_sync(0xffffffffu, hd);
     const int wi = j * (kTileThreads / 32) + warp;
     if (lane == 0 && wi < WORDS) s_head[wi] = hmask[j];
   }
   __syncthreads();
-  const long long t_2 = TKT_NOW();
   // ---- every warp: popcount prefix of the head words (redundant per warp: no extra barrier);
   //      each head row records itself at its local id ----
   int agg, ptot;
@@ -327,14 +413,27 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       if ((hmask[j] >> lane) & 1u) s_row[wex + __popc(hmask[j] & lt)] = (short)(j * kTileThreads + tid);
     }
   }
-  if (warp == 0 && lane == 0) {
+#ifdef TK_LAG0
+  if (warp == 0 && lane == 0) st_relaxed(p.status + tile, kStReady | (unsigned long long)agg);
+#endif
+  auto wait_prefix = [&]() {
     // ---- this tile's exclusive prefix (the scanner block published it ~lag tiles ago) ----
-    const unsigned long long excl = tile_wait_prefix(p.status, tile, (unsigned long long)agg);
+    unsigned long long excl = 0;
+#ifdef TK_DIAG_WAITSTAT  // diagnostics: tiles whose prefix was not ready at the first poll
+    if ((ld_relaxed(p.status + tile) >> 62) != 2) atomicAdd(&p.ctr->streamers_done, 1u);
+#endif
+    if (!tile_wait_prefix(p.status, tile, (unsigned long long)agg, pre, &excl)) {
+      tile_stall(p.ctr, 3, tile);
+      excl = ~0ull;  // no output from this tile
+    }
     s_base = excl;
     if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
-    TKT_ADD(2, TKT_NOW() - t_2);
-  }
-  unsigned int flags = 0;
+    TKR(3);
+  };
+#ifndef TK_LAG0
+  if (warp == 0 && lane == 0) wait_prefix();
+#endif
+  unsigned int flags = unsorted ? kFlagUnsorted : 0u;  // unsorted: rare, the host takes the sort path
   // ---- w = vals * x[subk] (all gathers in flight before any store) ----
   if constexpr (SRC == kSrcRaw) {
     double xv[ITER], av[ITER];
@@ -357,11 +456,15 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   }
   if (flags) atomicOr(&s_flags, flags);
+#ifdef TK_LAG0
+  if (warp == 0 && lane == 0) wait_prefix();
+#endif
   __syncthreads();  // w, the head rows and the base are ready
   if (tid == 0) {
     if (s_flags) atomicOr(&p.ctr->flags, s_flags);
-    TKT_ADD(1, TKT_NOW() - t_0);
+    TKR(4);
   }
+  if (s_base == ~0ull) return;  // watchdog: the call fails
   const long long base = (long long)s_base;
   // one group's output row: (kept key of its head row, folded value) at base + local id
   auto emit = [&](int li, int r, double v) {
@@ -404,8 +507,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   }
   __syncthreads();  // the long-group list and the open group are known
-  const long long t_3 = TKT_NOW();
-  if (tid == 0) TKT_ADD(3, t_3 - t_2);
+  if (tid == 0) TKR(5);
   // ---- longer closed groups: one per thread, packed into the first warps; a warp with nothing
   //      left exits here, so the SM can start another tile while the folds run ----
   const int nl = s_nlist;
@@ -420,12 +522,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   zeros = __reduce_add_sync(0xffffffffu, zeros);
   if (lane == 0 && zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
   if (tid == 0) {
-    TKT_ADD(4, TKT_NOW() - t_3);
-    TKT_ADD(6, 1);
-    if (open_li < 0) TKT_ADD(9, TKT_NOW() - t_0);
+    TKR(6);
   }
   if (warp != 0 || open_li < 0) return;
-  const long long t_4 = TKT_NOW();
 
   // ---- the group that runs past the halo, finished by warp 0 alone: 128-row chunks (L2-hot: the
   //      next tiles' CTAs read them), w staged in the free subk column; the next chunk's loads are
@@ -485,10 +584,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     for (int c = 0; c < NKR; ++c)
       if (NK > 0 || c < nk) k[c] = gk[c];
     seg_emit<SRC>(p, base + open_li, k, acc);
-    const long long t_5 = TKT_NOW();
-    TKT_ADD(5, t_5 - t_4);
-    TKT_ADD(7, 1);
-    TKT_ADD(9, t_5 - t_0);
+    TKR(7);
   }
 }
 

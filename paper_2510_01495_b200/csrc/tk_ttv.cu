@@ -360,6 +360,8 @@ void set_smem_once(K kernel, size_t bytes) {
   size_t& have = done[{reinterpret_cast<const void*>(kernel), dev}];
   if (bytes > have) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    // all shared memory: eight tile CTAs need ~216 KB; x's hot entries still fit the rest of L1
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     have = bytes;
   }
 }
@@ -379,7 +381,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   constexpr int HALO = 32;
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
-  const size_t smem = tile_smem_bytes<TILE, HALO>(ncol, nk) + (SRC == kSrcRaw ? 0 : (size_t)TILE * 8);
+  const size_t smem = tile_total_smem<SRC, TILE, HALO>(ncol, nk);
   auto kern = ttv_tile_kernel<SRC, NK, TILE, HALO>;
   set_smem_once(kern, smem);
   const long long ntiles = (p.n + TILE - 1) / TILE;
@@ -391,32 +393,46 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   p.ctr = reinterpret_cast<Counters*>(b + status_b);
   TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
   DevBuf prof;
-  const bool profile = getenv("TK_TILE_PROFILE") != nullptr;
-  if (profile) {
-    if (int rc = prof.alloc(16 * 8, st)) return rc;
-    TK_CUDA(cudaMemsetAsync(prof.get(), 0, 16 * 8, st));
+#ifdef TK_TRACE
+  const char* trace_file = getenv("TK_TRACE_FILE");
+  const unsigned nblk = (unsigned)(ntiles + std::min<long long>(1024, ntiles) + 1);
+  if (trace_file) {
+    if (int rc = prof.alloc((size_t)nblk * 64, st)) return rc;
+    TK_CUDA(cudaMemsetAsync(prof.get(), 0, (size_t)nblk * 64, st));
     p.prof = prof.as<unsigned long long>();
   }
+#endif
   ktimer_begin(st);
   // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
+#ifdef TK_LAG0
+  p.lag = 0;
+#else
   p.lag = std::min<long long>(1024, ntiles);
+#endif
   kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();
   TK_CUDA(cudaGetLastError());
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
-  if (profile) {
-    unsigned long long h[16];
-    TK_CUDA(cudaMemcpy(h, prof.get(), sizeof h, cudaMemcpyDeviceToHost));
-    const double nt = (double)std::max(1ull, h[6]), ns = (double)std::max(1ull, h[7]);
-    fprintf(stderr,
-            "[tk tile profile] tiles=%llu spills=%llu | per tile (us): data %.2f  w+heads %.2f  lookback %.2f  "
-            "folds+lb %.2f  output %.2f  life %.2f | per spill: %.2f us\n",
-            h[6], h[7], h[0] / nt / 1965.0, (h[1] - h[0]) / nt / 1965.0, h[2] / nt / 1965.0, h[3] / nt / 1965.0,
-            h[4] / nt / 1965.0, h[9] / nt / 1965.0, h[5] / ns / 1965.0);
+#ifdef TK_DIAG_WAITSTAT
+  fprintf(stderr, "[tk] tiles %lld, prefix not ready at first poll: %u\n", ntiles, host_ctr->streamers_done);
+#endif
+  if (host_ctr->flags & kFlagStall)
+    return fail(TK_ECUDA, "internal error: tile pipeline wait gave up (site " +
+                              std::to_string(host_ctr->q_head >> 56) + ", tile " +
+                              std::to_string(host_ctr->q_head & ((1ull << 56) - 1)) + ")");
+#ifdef TK_TRACE
+  if (trace_file) {
+    std::vector<unsigned long long> h((size_t)nblk * 8);
+    TK_CUDA(cudaMemcpy(h.data(), prof.get(), h.size() * 8, cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(trace_file, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
     p.prof = nullptr;
   }
+#endif
   return TK_OK;
 }
 

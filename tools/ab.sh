@@ -5,7 +5,7 @@ cp paper_2510_01495_b200/libtk_b200.so /tmp/tk_keep.so
 for v in variants/*.so; do
   cp "$v" paper_2510_01495_b200/libtk_b200.so
   for i in 1 2; do
-    python bench.py --steps 10 --warmup 3 --no-secondary --no-e2e --no-cpu "$@" 2>/dev/null |
+    timeout 120 python bench.py --steps 10 --warmup 3 --no-secondary --no-e2e --no-cpu "$@" 2>/dev/null |
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $v .so)', round(d['ms_per_step'],3), round(d['roofline']['kernel_ms'],3))"
   done
 done
