@@ -155,14 +155,23 @@ __device__ __forceinline__ double fold_run(const double* s_a, int j, int end, do
 #ifdef TK_DIAG_NOFOLD  // diagnostics only: wrong values, measures the cost of the serial folds
   return acc + (end > j ? s_a[end - 1] : 0.0);
 #endif
+  // 16-byte shared loads: half the shared-memory wavefronts of a serial fold
+  if ((j & 1) && j < end) acc = __dadd_rn(acc, s_a[j++]);
   for (; j + 4 <= end; j += 4) {
-    const double v0 = s_a[j], v1 = s_a[j + 1], v2 = s_a[j + 2], v3 = s_a[j + 3];
-    acc = __dadd_rn(acc, v0);
-    acc = __dadd_rn(acc, v1);
-    acc = __dadd_rn(acc, v2);
-    acc = __dadd_rn(acc, v3);
+    const double2 v01 = *reinterpret_cast<const double2*>(s_a + j);
+    const double2 v23 = *reinterpret_cast<const double2*>(s_a + j + 2);
+    acc = __dadd_rn(acc, v01.x);
+    acc = __dadd_rn(acc, v01.y);
+    acc = __dadd_rn(acc, v23.x);
+    acc = __dadd_rn(acc, v23.y);
   }
-  for (; j < end; ++j) acc = __dadd_rn(acc, s_a[j]);
+  if (j + 2 <= end) {
+    const double2 v01 = *reinterpret_cast<const double2*>(s_a + j);
+    acc = __dadd_rn(acc, v01.x);
+    acc = __dadd_rn(acc, v01.y);
+    j += 2;
+  }
+  if (j < end) acc = __dadd_rn(acc, s_a[j]);
   return acc;
 }
 

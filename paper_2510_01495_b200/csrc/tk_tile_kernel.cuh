@@ -271,11 +271,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // Each warp takes 128 consecutive rows; the previous row's key comes from the neighbouring lane
   // (lane 31 carries the row before the warp's first row, then the previous iteration's last row).
   // The order check (kept keys non-decreasing) lives here too, while the keys are in registers.
-#ifdef TK_LAG0  // the fold publishes its own aggregate: no separate count
-  if (false) {
-#else
   if (count_tile < ntiles) {
-#endif
     const long long cstart = count_tile * TILE;
     const int ccnt = (int)min((long long)TILE, p.n - cstart);
     const int wrow0 = warp * (TILE / kTileWarps);
@@ -413,15 +409,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       if ((hmask[j] >> lane) & 1u) s_row[wex + __popc(hmask[j] & lt)] = (short)(j * kTileThreads + tid);
     }
   }
-#ifdef TK_LAG0
-  if (warp == 0 && lane == 0) st_relaxed(p.status + tile, kStReady | (unsigned long long)agg);
-#endif
-  auto wait_prefix = [&]() {
+  if (warp == 0 && lane == 0) {
     // ---- this tile's exclusive prefix (the scanner block published it ~lag tiles ago) ----
     unsigned long long excl = 0;
-#ifdef TK_DIAG_WAITSTAT  // diagnostics: tiles whose prefix was not ready at the first poll
-    if ((ld_relaxed(p.status + tile) >> 62) != 2) atomicAdd(&p.ctr->streamers_done, 1u);
-#endif
     if (!tile_wait_prefix(p.status, tile, (unsigned long long)agg, pre, &excl)) {
       tile_stall(p.ctr, 3, tile);
       excl = ~0ull;  // no output from this tile
@@ -429,10 +419,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     s_base = excl;
     if (start + cnt == p.n) p.ctr->groups = excl + (unsigned long long)agg;
     TKR(3);
-  };
-#ifndef TK_LAG0
-  if (warp == 0 && lane == 0) wait_prefix();
-#endif
+  }
   unsigned int flags = unsorted ? kFlagUnsorted : 0u;  // unsorted: rare, the host takes the sort path
   // ---- w = vals * x[subk] (all gathers in flight before any store) ----
   if constexpr (SRC == kSrcRaw) {
@@ -456,9 +443,6 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   }
   if (flags) atomicOr(&s_flags, flags);
-#ifdef TK_LAG0
-  if (warp == 0 && lane == 0) wait_prefix();
-#endif
   __syncthreads();  // w, the head rows and the base are ready
   if (tid == 0) {
     if (s_flags) atomicOr(&p.ctr->flags, s_flags);

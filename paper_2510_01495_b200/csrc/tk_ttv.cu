@@ -404,20 +404,13 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
 #endif
   ktimer_begin(st);
   // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
-#ifdef TK_LAG0
-  p.lag = 0;
-#else
   p.lag = std::min<long long>(1024, ntiles);
-#endif
   kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();
   TK_CUDA(cudaGetLastError());
   TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
-#ifdef TK_DIAG_WAITSTAT
-  fprintf(stderr, "[tk] tiles %lld, prefix not ready at first poll: %u\n", ntiles, host_ctr->streamers_done);
-#endif
   if (host_ctr->flags & kFlagStall)
     return fail(TK_ECUDA, "internal error: tile pipeline wait gave up (site " +
                               std::to_string(host_ctr->q_head >> 56) + ", tile " +
