@@ -4,6 +4,7 @@
 // for unchecked calls (_check_ttv, pkg/src/tenkern/_ckernels.pyx:298-310): order >= 2,
 // 0 <= k < d, len(x) == shape[k]; messages use the reference's wording so the Python
 // layer can raise the same exception text.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <climits>
@@ -268,6 +269,123 @@ int tk_ttv_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_
   return ttv_sparse_device(d, shape, nnz, cp.data(), vals, x, nx, k, out_subs, out_vals, out_nnz, st);
 }
 
+constexpr int64_t kPipeRows = 16ll << 20;  // rows per chunk of the pipelined host TTV
+constexpr int kPipeDeclined = -1;          // the pipelined path does not apply: use the one-shot path
+
+cudaStream_t side_stream(int which) {  // 0: host->device copies, 1: device->host copies
+  static cudaStream_t s[64][2] = {};
+  const int dev = cur_dev();
+  if (!s[dev][which]) cudaStreamCreateWithFlags(&s[dev][which], cudaStreamNonBlocking);
+  return s[dev][which];
+}
+
+// kept key (first d-1 coordinates) of host rows i and j: -1 / 0 / +1 (lexicographic)
+int key_cmp(const int64_t* subs, int d, int64_t i, int64_t j) {
+  for (int c = 0; c < d - 1; ++c) {
+    const int64_t a = subs[i * d + c], b = subs[j * d + c];
+    if (a != b) return a < b ? -1 : 1;
+  }
+  return 0;
+}
+
+// Host-buffer TTV with k == d-1, pipelined over chunks cut at kept-key changes: the copy of chunk
+// i+1 in, the TTV of chunk i and the copy of chunk i-1's result out overlap (PCIe is full duplex),
+// so the call costs ~ the input transfer.  Each chunk is a complete set of groups, so the result
+// is the concatenation of the chunk results.  Declines (kPipeDeclined) if the input is not in
+// kept-key order -- the one-shot path then sorts.
+int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
+                       const double* x, int64_t nx, int64_t* out_subs, double* out_vals, int64_t* out_nnz) {
+  (void)shape;
+  const int nk = d - 1;
+  std::vector<int64_t> cut{0};
+  while (cut.back() < nnz) {
+    int64_t e = std::min(nnz, cut.back() + kPipeRows);
+    while (e < nnz && key_cmp(subs, d, e - 1, e) == 0) ++e;  // never split a group
+    if (e < nnz && key_cmp(subs, d, e - 1, e) > 0) return kPipeDeclined;
+    cut.push_back(e);
+  }
+  const int nchunk = (int)cut.size() - 1;
+  int64_t rows = 0;
+  for (int i = 0; i < nchunk; ++i) rows = std::max(rows, cut[i + 1] - cut[i]);
+  const int64_t pitch = pitch_of(rows);
+  cudaStream_t sc = lib_stream(), si = side_stream(0), so = side_stream(1);
+  DevBuf b_x, b_aos[2], b_soa[2], b_vals[2], b_os[2], b_ov[2];
+  if (int rc = b_x.alloc((size_t)std::max<int64_t>(nx, 1) * 8, sc)) return rc;
+  for (int b = 0; b < 2; ++b) {
+    if (int rc = b_aos[b].alloc((size_t)rows * d * 8, sc)) return rc;
+    if (int rc = b_soa[b].alloc((size_t)pitch * d * 8, sc)) return rc;
+    if (int rc = b_vals[b].alloc((size_t)rows * 8, sc)) return rc;
+    if (int rc = b_os[b].alloc((size_t)rows * nk * 8, sc)) return rc;
+    if (int rc = b_ov[b].alloc((size_t)rows * 8, sc)) return rc;
+  }
+  if (nx) TK_CUDA(cudaMemcpyAsync(b_x.get(), x, (size_t)nx * 8, cudaMemcpyHostToDevice, sc));
+  cudaEvent_t ev_in[2], ev_done[2], ev_free[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming);
+  }
+  struct Cleanup {
+    cudaEvent_t* e;
+    ~Cleanup() {
+      for (int i = 0; i < 6; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t all[6] = {ev_in[0], ev_in[1], ev_done[0], ev_done[1], ev_free[0], ev_free[1]};
+  Cleanup cleanup_{all};
+  struct Drain {  // on every exit: the side streams are done before the buffers go back to the pool
+    cudaStream_t a, b;
+    ~Drain() {
+      cudaStreamSynchronize(a);
+      cudaStreamSynchronize(b);
+    }
+  } drain_{si, so};
+  // the pool allocations above are stream-ordered on sc: the side streams start after them
+  TK_CUDA(cudaEventRecord(ev_done[0], sc));
+  TK_CUDA(cudaStreamWaitEvent(si, ev_done[0], 0));
+  TK_CUDA(cudaStreamWaitEvent(so, ev_done[0], 0));
+  auto copy_in = [&](int i) -> int {
+    const int b = i & 1;
+    const int64_t n = cut[i + 1] - cut[i];
+    TK_CUDA(cudaMemcpyAsync(b_aos[b].get(), subs + cut[i] * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, si));
+    TK_CUDA(cudaMemcpyAsync(b_vals[b].get(), vals + cut[i], (size_t)n * 8, cudaMemcpyHostToDevice, si));
+    TK_CUDA(cudaEventRecord(ev_in[b], si));
+    return TK_OK;
+  };
+  if (int rc = copy_in(0)) return rc;
+  int64_t off = 0;
+  for (int i = 0; i < nchunk; ++i) {
+    const int b = i & 1;
+    const int64_t n = cut[i + 1] - cut[i];
+    if (i + 1 < nchunk) {  // the other buffer set is free once chunk i-1's TTV has run (host-synced)
+      if (int rc = copy_in(i + 1)) return rc;
+    }
+    TK_CUDA(cudaStreamWaitEvent(sc, ev_in[b], 0));
+    if (i >= 2) TK_CUDA(cudaStreamWaitEvent(sc, ev_free[b], 0));  // chunk i-2's result copied out
+    if (int rc = aos_to_soa(n, d, b_aos[b].as<int64_t>(), b_soa[b].as<int64_t>(), pitch, sc)) return rc;
+    std::vector<const int64_t*> cp(d);
+    for (int m = 0; m < d; ++m) cp[m] = b_soa[b].as<int64_t>() + (size_t)m * pitch;
+    int64_t u = 0;
+    bool unsorted = false;
+    if (int rc = ttv_prefix_try(d, n, cp.data(), b_vals[b].as<double>(), b_x.as<double>(), nx, b_os[b].as<int64_t>(),
+                                b_ov[b].as<double>(), &u, &unsorted, sc))
+      return rc;
+    if (unsorted) return kPipeDeclined;
+    TK_CUDA(cudaEventRecord(ev_done[b], sc));
+    TK_CUDA(cudaStreamWaitEvent(so, ev_done[b], 0));
+    if (u) {
+      TK_CUDA(cudaMemcpyAsync(out_subs + off * nk, b_os[b].get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, so));
+      TK_CUDA(cudaMemcpyAsync(out_vals + off, b_ov[b].get(), (size_t)u * 8, cudaMemcpyDeviceToHost, so));
+    }
+    TK_CUDA(cudaEventRecord(ev_free[b], so));
+    off += u;
+  }
+  TK_CUDA(cudaStreamSynchronize(so));
+  TK_CUDA(cudaStreamSynchronize(sc));
+  *out_nnz = off;
+  return TK_OK;
+}
+
 int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
                     const double* x, int64_t nx, int32_t k, int64_t* out_subs, double* out_vals, int64_t* out_nnz) {
   CallClock clock_;
@@ -275,6 +393,11 @@ int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t*
   if (nnz < 0 || out_nnz == nullptr) return fail(TK_EARG, "ttv: bad nnz / out_nnz");
   *out_nnz = 0;
   if (nnz == 0) return TK_OK;
+  if (k == d - 1 && nnz >= 2 * kPipeRows) {
+    const int rc = ttv_host_pipelined(d, shape, nnz, subs, vals, x, nx, out_subs, out_vals, out_nnz);
+    if (rc != kPipeDeclined) return rc;
+    *out_nnz = 0;
+  }
   cudaStream_t st = lib_stream();
   const int64_t pitch = pitch_of(nnz);
   const int nk = d - 1;

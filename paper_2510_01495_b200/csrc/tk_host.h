@@ -66,6 +66,10 @@ void ktimer_end(cudaStream_t st);
 void count_launch(int n = 1);
 
 // sparse-result TTV on device-resident SoA data (cols[m] device pointers, m < d).
+// Prefix-kept TTV (k == d-1) over device SoA columns without the sort fallback: *unsorted is set
+// (and nothing written) when the kept keys are not non-decreasing.
+int ttv_prefix_try(int d, int64_t nnz, const int64_t* const* cols, const double* vals, const double* x, int64_t nx,
+                   int64_t* out_subs, double* out_vals, int64_t* out_nnz, bool* unsorted, cudaStream_t st);
 int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
                       const double* x, int64_t nx, int k, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
                       cudaStream_t st, bool keep_zeros = false);

@@ -601,6 +601,35 @@ int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const
 
 }  // namespace
 
+int ttv_prefix_try(int d, int64_t nnz, const int64_t* const* cols, const double* vals, const double* x, int64_t nx,
+                   int64_t* out_subs, double* out_vals, int64_t* out_nnz, bool* unsorted, cudaStream_t st) {
+  *out_nnz = 0;
+  *unsorted = false;
+  if (nnz == 0) return TK_OK;
+  const int nk = d - 1, k = d - 1;
+  SegParams p{};
+  p.n = nnz;
+  p.nk = nk;
+  for (int c = 0; c < nk; ++c) p.key[c] = reinterpret_cast<const long long*>(cols[c]);
+  p.subk = reinterpret_cast<const long long*>(cols[k]);
+  p.a = vals;
+  p.x = x;
+  p.nx = nx;
+  p.out_nk = nk;
+  p.out_subs = reinterpret_cast<long long*>(out_subs);
+  p.out_vals = out_vals;
+  bool al = aligned16(vals) && aligned16(p.subk);
+  for (int c = 0; c < nk; ++c) al = al && aligned16(p.key[c]);
+  p.bulk_ok = al;
+  Counters c{};
+  if (int rc = run_seg(kSrcRaw, p, st, &c)) return rc;
+  if ((c.flags & kFlagUnsorted) && !(c.flags & kFlagIndex)) {
+    *unsorted = true;
+    return TK_OK;
+  }
+  return finish(c, k, nx, nk, p.out_subs, out_vals, out_nnz, st);
+}
+
 int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
                       const double* x, int64_t nx, int k, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
                       cudaStream_t st, bool keep_zeros) {

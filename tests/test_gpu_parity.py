@@ -299,3 +299,58 @@ def test_dense_multi_vector_ttv(oracle):
     s2, v2 = small.to_host()
     r = oracle.ttv_multi_dense(s2, v2, small.shape, {m: v.cpu().numpy() for m, v in vv.items()}, 0)
     assert np.max(np.abs(o - r) / np.abs(r)) <= REL
+
+
+def _host_ttv(subs, vals, shape, x, k):
+    """tk_ttv_f64_host straight through the C ABI (the pipelined path for k == d-1, >= 32M rows)."""
+    import ctypes
+    from paper_2510_01495_b200 import _lib
+    n, d = subs.shape
+    os_ = np.empty((n, d - 1), dtype=np.int64)
+    ov = np.empty(n, dtype=np.float64)
+    u = ctypes.c_int64(0)
+    _lib.check(_lib.load().tk_ttv_f64_host(d, _lib.i64_array(shape), n, subs.ctypes.data, vals.ctypes.data,
+                                           x.ctypes.data, len(x), k, os_.ctypes.data, ov.ctypes.data,
+                                           ctypes.byref(u)))
+    return os_[:u.value], ov[:u.value]
+
+
+def test_host_pipeline_chunks_match_device_path():
+    """>= 32M rows, k == d-1: the host call runs in key-aligned chunks with overlapped copies;
+    the result must be bit-identical to the one-shot device path (itself oracle-checked)."""
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (200000, 3000, 5000)
+    t = DeviceCoo.generate(shape, 40_000_000, zipf_s=1.2, normal_vals=True, seed=2024)
+    x = uniform_vector(shape[2], 11)
+    u, os_d, ov_d = t.ttv(x, 2)
+    subs, vals = t.to_host()
+    s, v = _host_ttv(np.ascontiguousarray(subs), np.ascontiguousarray(vals), shape, x.cpu().numpy(), 2)
+    assert len(v) == u
+    assert s.tobytes() == os_d[:u].cpu().numpy().tobytes()
+    assert v.tobytes() == ov_d[:u].cpu().numpy().tobytes()
+
+
+def test_host_pipeline_declines_unsorted_and_reports_index_errors():
+    from paper_2510_01495_b200 import errors
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (100000, 3000, 5000)
+    t = DeviceCoo.generate(shape, 34_000_000, zipf_s=1.1, normal_vals=True, seed=77)
+    x = uniform_vector(shape[2], 3)
+    u, os_d, ov_d = t.ttv(x, 2)
+    subs, vals = t.to_host()
+    subs = np.ascontiguousarray(subs)
+    vals = np.ascontiguousarray(vals)
+    # reversed row order: not in kept-key order -> the pipelined path declines, the sort path runs
+    rs, rv = subs[::-1].copy(), vals[::-1].copy()
+    s, v = _host_ttv(rs, rv, shape, x.cpu().numpy(), 2)
+    assert len(v) == u and s.tobytes() == os_d[:u].cpu().numpy().tobytes()
+    # the reference folds in original row order: reversed input folds each group in reverse
+    # order, so compare against the device path on the same reversed rows
+    tr = DeviceCoo.from_host(rs, rv, shape)
+    u2, _, ov2 = tr.ttv(x, 2)
+    assert v.tobytes() == ov2[:u2].cpu().numpy().tobytes()
+    # an out-of-range contracted index in a late chunk -> DimensionError, like the reference
+    bad = subs.copy()
+    bad[-5, 2] = shape[2]
+    with pytest.raises(errors.DimensionError):
+        _host_ttv(bad, vals, shape, x.cpu().numpy(), 2)
