@@ -435,7 +435,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nnz", type=int, default=0, help="override config-5 nnz (debug only)")
-    ap.add_argument("--cpu-sample", type=int, default=40_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=320_000_000,
+                    help="rows of the config-5 prefix the CPU legs time (~10 s per call)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
