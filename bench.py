@@ -345,7 +345,7 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        if tj.get("nnz") == n_local and tj.get("kernel") == "ttv_tile_kernel<Raw,2,512,32>":
+        if tj.get("nnz") == n_local and tj.get("kernel") == "ttv_tile_kernel<Raw,2,768,32>":
             traffic = tj.get("dram_bytes_per_launch")
 
     # ---- e2e through the host-buffer C ABI (pinned host in, host out) ----
@@ -377,7 +377,7 @@ def run_ours(args):
                        "l2": "inputs (12.8 GB) larger than L2; no flush", "gen_seconds": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "ttv_tile_kernel<Raw,2,512,32>", "kernel_ms": kern_ms,
+                         "kernel": "ttv_tile_kernel<Raw,2,768,32>", "kernel_ms": kern_ms,
                          "alg_bytes_per_launch": alg_bytes},
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),

@@ -26,6 +26,9 @@ namespace tk {
 #ifndef TK_TILE_PF
 #define TK_TILE_PF 256  // tiles ahead of the count whose columns are prefetched into L2
 #endif
+#ifndef TK_TILE_PFV
+#define TK_TILE_PFV 64  // tiles ahead of the fold whose value columns are prefetched into L2
+#endif
 #ifndef TK_SCAN_D
 #define TK_SCAN_D 8  // status words per scanner lane per round
 #endif
@@ -252,11 +255,12 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
 
   __syncthreads();  // the mbarrier is initialised and the tile's copies are issued
 
-  // ---- L2 prefetch of every column of tile count_tile + TK_TILE_PF: the count loads of that tile
-  //      and, ~lag tiles later, its fold's TMA then hit L2; HBM sees only these async requests ----
+  // ---- L2 prefetch: the key columns of tile count_tile + TK_TILE_PF (the count's loads, and ~lag
+  //      tiles later the fold's copy, then hit L2) and the value columns of tile fold_tile +
+  //      TK_TILE_PFV (close to their use, so they do not crowd L2); HBM sees these async requests ----
   if (TK_TILE_PF > 0 && warp == 1 && lane < ncol) {
-    const long long pt = count_tile + TK_TILE_PF;
-    if (pt < ntiles) {
+    const long long pt = lane < nk ? count_tile + TK_TILE_PF : fold_tile + TK_TILE_PFV;
+    if (pt >= 0 && pt < ntiles) {
       const long long ps = pt * TILE;
       const uint32_t bytes = (uint32_t)(min((long long)TILE, p.n - ps) * 8) & ~15u;
       const void* src = lane < nk ? (const void*)(p.key[lane] + ps)
@@ -266,6 +270,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
     }
   }
+
 
   // ---- count the heads of tile count_tile straight from global memory, publish the aggregate ----
   // Each warp takes 128 consecutive rows; the previous row's key comes from the neighbouring lane

@@ -377,7 +377,13 @@ int grid_for(long long n, int per_thread = 4) {
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   // one CTA per tile, eight CTAs per SM (~19 KB shared memory each: L1 keeps x resident)
-  constexpr int TILE = NK > 0 ? 512 : 256;
+#ifndef TK_TILE_LAG
+#define TK_TILE_LAG 1024  // tiles between a tile's count and its fold
+#endif
+#ifndef TK_TILE_ROWS
+#define TK_TILE_ROWS 768
+#endif
+  constexpr int TILE = NK > 0 ? TK_TILE_ROWS : 256;
   constexpr int HALO = 32;
   const int nk = SRC == kSrcLinKey ? 1 : p.nk;
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
@@ -395,7 +401,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   DevBuf prof;
 #ifdef TK_TRACE
   const char* trace_file = getenv("TK_TRACE_FILE");
-  const unsigned nblk = (unsigned)(ntiles + std::min<long long>(1024, ntiles) + 1);
+  const unsigned nblk = (unsigned)(ntiles + std::min<long long>(TK_TILE_LAG, ntiles) + 1);
   if (trace_file) {
     if (int rc = prof.alloc((size_t)nblk * 64, st)) return rc;
     TK_CUDA(cudaMemsetAsync(prof.get(), 0, (size_t)nblk * 64, st));
@@ -404,7 +410,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
 #endif
   ktimer_begin(st);
   // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
-  p.lag = std::min<long long>(1024, ntiles);
+  p.lag = std::min<long long>(TK_TILE_LAG, ntiles);
   kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();

@@ -59,7 +59,7 @@ def gb(k):
     v = float(d[k])
     return v * {"Gbyte": 1e9, "GB": 1e9, "Mbyte": 1e6, "MB": 1e6, "Kbyte": 1e3, "KB": 1e3, "byte": 1, "B": 1}[units[k]]
 ms = float(d["gpu__time_duration.sum"]) * {"msecond": 1, "ms": 1, "usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6, "ns": 1e-6}[units["gpu__time_duration.sum"]]
-kname = "ttv_tile_kernel<Raw,2,512,32>"
+kname = "ttv_tile_kernel<Raw,2,768,32>"
 json.dump({"kernel": kname, "nnz": 400000000, "workload": "cfg5 (4e8 nnz Zipf, mode 2)",
            "dram_bytes_read": gb("dram__bytes_read.sum"), "dram_bytes_write": gb("dram__bytes_write.sum"),
            "dram_bytes_per_launch": gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum"),
