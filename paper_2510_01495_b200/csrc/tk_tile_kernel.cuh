@@ -68,7 +68,7 @@ constexpr int tile_list_cap() {  // closed groups longer than kTileShort rows pe
 // precomputed-w sources, which have no subk column to reuse)
 template <int TILE, int HALO>
 constexpr size_t tile_smem_bytes(int ncol, int nk) {
-  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2 + (size_t)tile_list_cap<TILE>() * 8;
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2 + (size_t)tile_list_cap<TILE>() * 4;
 }
 
 template <int SRC, int TILE, int HALO>
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   constexpr int WORDS = ROWS / 32;
   constexpr int ITER = (ROWS + kTileThreads - 1) / kTileThreads;
   constexpr int NKR = NK > 0 ? NK : kMaxKeep;
-  static_assert(ROWS % 32 == 0 && WORDS <= 32 && TILE % 32 == 0, "tile geometry");
+  static_assert(ROWS % 32 == 0 && WORDS <= 32 && TILE % 32 == 0 && ROWS <= 1024, "tile geometry");
   const int nk = seg_nk<SRC, NK>(p);
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);  // keys | a | subk
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // folded values by local id reuse the subk column (free once w is formed); for the
   // precomputed-w sources there is no subk column, so they get their own area
   short* s_row = reinterpret_cast<short*>(s_prev2 + 2 * nk);
-  unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_row + ROWS);
+  unsigned int* s_list = reinterpret_cast<unsigned int*>(s_row + ROWS);  // end << 20 | row << 10 | id
   double* s_val =
       SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : reinterpret_cast<double*>(s_list + tile_list_cap<TILE>());
 
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       zeros += v == 0.0;
     } else {
       const int q = atomicAdd(&s_nlist, 1);
-      s_list[q] = ((unsigned long long)end << 32) | ((unsigned long long)r << 16) | (unsigned long long)li;
+      s_list[q] = ((unsigned int)end << 20) | ((unsigned int)r << 10) | (unsigned int)li;
     }
   }
   __syncthreads();  // the long-group list and the open group are known
@@ -502,8 +502,8 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   const int nl = s_nlist;
   const int open_li = s_open_li;
   for (int q = tid; q < nl; q += kTileThreads) {
-    const unsigned long long e = s_list[q];
-    const int li = (int)(e & 0xffff), r = (int)((e >> 16) & 0xffff), end = (int)(e >> 32);
+    const unsigned int e = s_list[q];
+    const int li = (int)(e & 1023u), r = (int)((e >> 10) & 1023u), end = (int)(e >> 20);
     const double v = fold_run(s_a, r + 1, end, s_a[r]);
     emit(li, r, v);
     zeros += v == 0.0;
