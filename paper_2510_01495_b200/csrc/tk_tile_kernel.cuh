@@ -253,7 +253,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   }
 
-  __syncthreads();  // the mbarrier is initialised and the tile's copies are issued
+  // warp 0 publishes "mbarrier initialised, copies issued, shared fields set" on named barrier 3;
+  // the other warps pick it up only before they touch the fold tile, so their count starts now
+  if (warp == 0 && fold_tile >= 0 && fold_tile < ntiles) named_arrive(3, kTileThreads);
 
   // ---- L2 prefetch: the key columns of tile count_tile + TK_TILE_PF (the count's loads, and ~lag
   //      tiles later the fold's copy, then hit L2) and the value columns of tile fold_tile +
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     if (tid == 0) TKR(1);
   }
   if (fold_tile < 0 || fold_tile >= ntiles) return;
+  if (warp != 0) named_bar(3, kTileThreads);
   const long long tile = s_tile;
   const long long start = tile * TILE;
   const int cnt = (int)min((long long)TILE, p.n - start);
