@@ -373,22 +373,21 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   unsigned int hmask[ITER];
   bool unsorted = false;
 #pragma unroll
-  for (int j = 0; j < ITER; ++j) {
+  for (int j = 0; j < ITER; ++j) {  // branch-free: rows past the stage load a clamped row
     const int r = j * kTileThreads + tid;
-    bool hd = false;
-    if (r < avail) {
-      bool less = false;
+    const int rc = min(r, ROWS - 1);
+    bool hd = false, less = false;
 #pragma unroll
-      for (int c = 0; c < NKR; ++c) {
-        if (NK == 0 && c >= nk) break;
-        const long long va = s_key[c * ROWS + r];
-        const long long vb = r ? s_key[c * ROWS + r - 1] : s_prev2[2 * c + 1];
-        less = less || (!hd && va < vb);
-        hd = hd || va != vb;
-      }
-      if (r == 0 && start == 0) hd = true;
-      else unsorted = unsorted || (less && r < cnt);
+    for (int c = 0; c < NKR; ++c) {
+      if (NK == 0 && c >= nk) break;
+      const long long va = s_key[c * ROWS + rc];
+      const long long vb = *(rc ? s_key + c * ROWS + rc - 1 : s_prev2 + 2 * c + 1);
+      less = less || (!hd && va < vb);
+      hd = hd || va != vb;
     }
+    const bool first = r == 0 && start == 0;
+    unsorted = unsorted || (less && !first && r < cnt);
+    hd = r < avail && (hd || first);
     hmask[j] = __ballot_sync(0xffffffffu, hd);
     const int wi = j * (kTileThreads / 32) + warp;
     if (lane == 0 && wi < WORDS) s_head[wi] = hmask[j];
@@ -433,16 +432,14 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   if constexpr (SRC == kSrcRaw) {
     double xv[ITER], av[ITER];
 #pragma unroll
-    for (int j = 0; j < ITER; ++j) {
+    for (int j = 0; j < ITER; ++j) {  // branch-free: rows past the stage gather x[0]
       const int r = j * kTileThreads + tid;
-      xv[j] = 0.0;
-      av[j] = 0.0;
-      if (r < avail) {
-        const long long idx = s_subk[r];
-        av[j] = s_a[r];
-        if ((unsigned long long)idx >= (unsigned long long)p.nx) flags |= kFlagIndex;
-        else xv[j] = __ldg(p.x + idx);
-      }
+      const int rc = min(r, ROWS - 1);
+      const long long idx = s_subk[rc];
+      av[j] = s_a[rc];
+      const bool bad = (unsigned long long)idx >= (unsigned long long)p.nx;
+      if (bad && r < avail) flags |= kFlagIndex;
+      xv[j] = __ldg(p.x + (bad ? 0 : idx));
     }
 #pragma unroll
     for (int j = 0; j < ITER; ++j) {
