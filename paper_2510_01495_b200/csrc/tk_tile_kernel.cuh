@@ -57,23 +57,16 @@ constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kStWarpShift = 56;
 constexpr unsigned long long kStCntMask = (1ull << kStWarpShift) - 1;
 constexpr unsigned long long kStReady = (unsigned long long)kTileWarps << kStWarpShift;
-constexpr int kTileShort = 8;  // folded inline by the classifying thread
-
-template <int TILE>
-constexpr int tile_list_cap() {  // closed groups longer than kTileShort rows per tile (+ slack)
-  return ((TILE / (kTileShort + 1) + 8) + 15) & ~15;
-}
-
-// stage columns + previous-row words + head-row ids + long-group list (+ value area for the
+// stage columns + previous-row words + head-row ids (+ the spill's 128-row chunk buffer for the
 // precomputed-w sources, which have no subk column to reuse)
 template <int TILE, int HALO>
 constexpr size_t tile_smem_bytes(int ncol, int nk) {
-  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2 + (size_t)tile_list_cap<TILE>() * 4;
+  return ((size_t)ncol * (TILE + HALO) + 2 * nk) * 8 + (size_t)(TILE + HALO) * 2;
 }
 
 template <int SRC, int TILE, int HALO>
 constexpr size_t tile_total_smem(int ncol, int nk) {
-  return tile_smem_bytes<TILE, HALO>(ncol, nk) + (SRC == kSrcRaw ? 0 : (size_t)TILE * 8);
+  return tile_smem_bytes<TILE, HALO>(ncol, nk) + (SRC == kSrcRaw ? 0 : (size_t)128 * 8);
 }
 
 __device__ __forceinline__ void named_arrive(int id, int threads) {
@@ -183,16 +176,14 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // folded values by local id reuse the subk column (free once w is formed); for the
   // precomputed-w sources there is no subk column, so they get their own area
   short* s_row = reinterpret_cast<short*>(s_prev2 + 2 * nk);
-  unsigned int* s_list = reinterpret_cast<unsigned int*>(s_row + ROWS);  // end << 20 | row << 10 | id
   double* s_val =
-      SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : reinterpret_cast<double*>(s_list + tile_list_cap<TILE>());
+      SRC == kSrcRaw ? reinterpret_cast<double*>(s_subk) : reinterpret_cast<double*>(s_row + ROWS);
 
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ long long s_tile;
   __shared__ int s_bulk;
   __shared__ unsigned int s_head[WORDS];
   __shared__ unsigned long long s_base;
-  __shared__ int s_nlist, s_open_li, s_open_r;
   __shared__ unsigned int s_flags;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -215,8 +206,6 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   if (tid == 0 && fold_tile >= 0) {
     const long long tile = fold_tile;
     s_tile = tile;
-    s_nlist = 0;
-    s_open_li = -1;
     s_flags = 0;
     const long long start = tile * TILE;
     const long long avail = min((long long)ROWS, p.n - start);
@@ -476,49 +465,30 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     }
   };
 
-  // ---- classify every group headed in the tile (striped: consecutive lanes write consecutive
-  //      output rows); short groups are folded and written at once ----
+  // ---- fold and write every group headed in the tile that closes inside the stage, one group
+  //      per thread, striped (consecutive lanes write consecutive output rows); a warp with
+  //      nothing left exits, so the SM can start another tile while long folds run.  The last
+  //      group is open (continues past the stage) iff the halo has no head and the stream goes
+  //      on -- every thread knows that without a barrier. ----
+  const int open_li = (agg > 0 && agg == ptot && start + avail < p.n) ? agg - 1 : -1;
   unsigned int zeros = 0;
   for (int li = tid; li < agg; li += kTileThreads) {
+    if (li == open_li) continue;
     const int r = s_row[li];
-    const bool last = li + 1 >= ptot;  // no later head in the stage
-    const int end = last ? avail : s_row[li + 1];
-    if (last && start + avail < p.n) {
-      s_open_li = li;
-      s_open_r = r;
-    } else if (end - r <= kTileShort) {
-      const double v = fold_run(s_a, r + 1, end, s_a[r]);
-      emit(li, r, v);
-      zeros += v == 0.0;
-    } else {
-      const int q = atomicAdd(&s_nlist, 1);
-      s_list[q] = ((unsigned int)end << 20) | ((unsigned int)r << 10) | (unsigned int)li;
-    }
-  }
-  __syncthreads();  // the long-group list and the open group are known
-  if (tid == 0) TKR(5);
-  // ---- longer closed groups: one per thread, packed into the first warps; a warp with nothing
-  //      left exits here, so the SM can start another tile while the folds run ----
-  const int nl = s_nlist;
-  const int open_li = s_open_li;
-  for (int q = tid; q < nl; q += kTileThreads) {
-    const unsigned int e = s_list[q];
-    const int li = (int)(e & 1023u), r = (int)((e >> 10) & 1023u), end = (int)(e >> 20);
+    const int end = li + 1 < ptot ? s_row[li + 1] : avail;
     const double v = fold_run(s_a, r + 1, end, s_a[r]);
     emit(li, r, v);
     zeros += v == 0.0;
   }
   zeros = __reduce_add_sync(0xffffffffu, zeros);
   if (lane == 0 && zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
-  if (tid == 0) {
-    TKR(6);
-  }
+  if (tid == 0) TKR(6);
   if (warp != 0 || open_li < 0) return;
 
   // ---- the group that runs past the halo, finished by warp 0 alone: 128-row chunks (L2-hot: the
   //      next tiles' CTAs read them), w staged in the free subk column; the next chunk's loads are
   //      in flight while lane 0 folds the current one ----
-  const int r0 = s_open_r;
+  const int r0 = s_row[open_li];
   long long gk[NKR];
 #pragma unroll
   for (int c = 0; c < NKR; ++c)
