@@ -78,10 +78,11 @@ __device__ __forceinline__ void named_arrive(int id, int threads) {
 // already-published aggregates in the next 32*D tiles (one L2 round trip), scans it, publishes the
 // prefixes and advances.  A tile therefore waits ~one round trip after its own aggregate, and
 // polls only its own status word -- no wide look-back windows hammering L2.
-// A wait that gives up records where (Counters::q_head = site << 56 | tile) and raises kFlagStall.
+// A wait that gives up raises kFlagStall; the first one records where (Counters::grab_ticket =
+// site, tile_ticket = tile).
 __device__ __forceinline__ void tile_stall(Counters* ctr, unsigned long long site, long long tile) {
+  if (atomicCAS(&ctr->grab_ticket, 0u, (unsigned int)site) == 0u) atomicExch(&ctr->tile_ticket, (unsigned int)tile);
   atomicOr(&ctr->flags, kFlagStall);
-  atomicExch(&ctr->q_head, (site << 56) | (unsigned long long)tile);
 }
 
 template <int D>

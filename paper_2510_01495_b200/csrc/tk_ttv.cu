@@ -419,8 +419,8 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   TK_CUDA(cudaStreamSynchronize(st));
   if (host_ctr->flags & kFlagStall)
     return fail(TK_ECUDA, "internal error: tile pipeline wait gave up (site " +
-                              std::to_string(host_ctr->q_head >> 56) + ", tile " +
-                              std::to_string(host_ctr->q_head & ((1ull << 56) - 1)) + ")");
+                              std::to_string(host_ctr->grab_ticket) + ", tile " +
+                              std::to_string(host_ctr->tile_ticket) + ")");
 #ifdef TK_TRACE
   if (trace_file) {
     std::vector<unsigned long long> h((size_t)nblk * 8);
