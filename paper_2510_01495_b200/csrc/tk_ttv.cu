@@ -182,7 +182,7 @@ __device__ __forceinline__ SegPair seg_combine(SegPair a, SegPair b) {
   return {a.f | b.f, b.f ? b.v : __dadd_rn(a.v, b.v)};
 }
 
-template <int kItems>
+template <int kItems, int D>  // D: tensor order when 3..5 (gathers batched), 0: any order
 __global__ void __launch_bounds__(256) dense_ttv_kernel(DenseParams p) {
   constexpr int TILE = kItems * 256;
   constexpr int NW = TILE / 32;
@@ -235,17 +235,42 @@ __global__ void __launch_bounds__(256) dense_ttv_kernel(DenseParams p) {
   // w = ((vals * x_{d-1}) * x_{d-2}) ... (descending modes: the chained-TTV association)
   unsigned int flags = 0;
   const long long nkeep = p.dims[keep];
+  // every gather of the tile in flight before the first multiply (D known at compile time)
+  double xg[D > 0 ? kItems : 1][D > 0 ? D : 1];
+  if constexpr (D > 0) {
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int r = j * 256 + tid;
+      const int rc = min(r, cnt - 1);
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        xg[j][m] = 1.0;
+        if (m != keep) {
+          const long long idx = s_col[m * TILE + rc];
+          const bool bad = (unsigned long long)idx >= (unsigned long long)p.dims[m];
+          if (bad && r < cnt) flags |= kFlagIndex;  // the call raises; the value is never used
+          xg[j][m] = __ldg(p.vec[m] + (bad ? 0 : idx));
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int r = j * 256 + tid;
     bool head = false;
     if (r < cnt) {
       double w = s_v[r];
-      for (int m = p.d - 1; m >= 0; --m) {
-        if (m == keep) continue;
-        const long long idx = s_col[m * TILE + r];
-        if (idx < 0 || idx >= p.dims[m]) { flags |= kFlagIndex; w = 0.0; }
-        else w = __dmul_rn(w, __ldg(p.vec[m] + idx));
+      if constexpr (D > 0) {
+#pragma unroll
+        for (int m = D - 1; m >= 0; --m)
+          if (m != keep) w = __dmul_rn(w, xg[j][m]);
+      } else {
+        for (int m = p.d - 1; m >= 0; --m) {
+          if (m == keep) continue;
+          const long long idx = s_col[m * TILE + r];
+          if (idx < 0 || idx >= p.dims[m]) { flags |= kFlagIndex; w = 0.0; }
+          else w = __dmul_rn(w, __ldg(p.vec[m] + idx));
+        }
       }
       s_v[r] = w;
       const long long key = s_key[r];
@@ -724,7 +749,8 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     p.bulk_ok = al;
     TK_CUDA(cudaMemsetAsync(p.ctr, 0, sizeof(Counters), st));
     const size_t smem = (size_t)(d + 1) * TILE * 8;
-    auto kern = dense_ttv_kernel<kItems>;
+    auto kern = d == 3 ? dense_ttv_kernel<kItems, 3> : d == 4 ? dense_ttv_kernel<kItems, 4>
+                : d == 5 ? dense_ttv_kernel<kItems, 5> : dense_ttv_kernel<kItems, 0>;
     set_smem_once(kern, smem);
     ktimer_begin(st);
     kern<<<(unsigned)ntiles, 256, smem, st>>>(p);
