@@ -364,6 +364,10 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   bool unsorted = false;
 #pragma unroll
   for (int j = 0; j < ITER; ++j) {  // branch-free: rows past the stage load a clamped row
+    if (j * kTileThreads + warp * 32 >= ROWS) {  // warp-uniform: this warp's rows are past the stage
+      hmask[j] = 0;
+      continue;
+    }
     const int r = j * kTileThreads + tid;
     const int rc = min(r, ROWS - 1);
     bool hd = false, less = false;
@@ -423,6 +427,10 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     double xv[ITER], av[ITER];
 #pragma unroll
     for (int j = 0; j < ITER; ++j) {  // branch-free: rows past the stage gather x[0]
+      if (j * kTileThreads + warp * 32 >= ROWS) {  // warp-uniform: past the stage
+        xv[j] = av[j] = 0.0;
+        continue;
+      }
       const int r = j * kTileThreads + tid;
       const int rc = min(r, ROWS - 1);
       const long long idx = s_subk[rc];
