@@ -466,6 +466,12 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
         lin /= dm;
       }
     } else {
+      if constexpr (NK == 2) {
+        if (p.out_v2) {  // one 16-byte store of the key pair
+          *reinterpret_cast<longlong2*>(p.out_subs + 2 * g) = make_longlong2(s_key[r], s_key[ROWS + r]);
+          return;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;

@@ -436,6 +436,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   ktimer_begin(st);
   // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
   p.lag = std::min<long long>(TK_TILE_LAG, ntiles);
+  p.out_v2 = p.out_nk == 2 && aligned16(p.out_subs);
   kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
   count_launch();

@@ -52,6 +52,7 @@ struct SegParams {
   int bulk_ok;                       // all stream pointers 16-byte aligned
   unsigned long long* prof;          // optional phase counters (TK_TILE_PROFILE=1), else null
   long long lag;                     // tile kernel: block b counts tile b-1 and folds tile b-1-lag
+  int out_v2;                        // out_nk == 2 and out_subs 16-byte aligned: one 16-byte key store
 };
 
 // development instrumentation: clock64 deltas summed over CTAs (off unless p.prof != null)
