@@ -182,175 +182,208 @@ __device__ __forceinline__ SegPair seg_combine(SegPair a, SegPair b) {
   return {a.f | b.f, b.f ? b.v : __dadd_rn(a.v, b.v)};
 }
 
-template <int kItems, int D>  // D: tensor order when 3..5 (gathers batched), 0: any order
-__global__ void __launch_bounds__(256) dense_ttv_kernel(DenseParams p) {
-  constexpr int TILE = kItems * 256;
-  constexpr int NW = TILE / 32;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  long long* s_col = reinterpret_cast<long long*>(smem_raw);   // [d][TILE]
-  double* s_v = reinterpret_cast<double*>(s_col + (size_t)p.d * TILE);
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ unsigned int s_head[NW];
-  __shared__ long long s_prev, s_next;
-  __shared__ int s_has_prev, s_has_next;
-  __shared__ SegPair s_warp[8];
-  __shared__ unsigned int s_flags;
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;  // identical in every lane (RN addition commutes)
+}
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long tile = blockIdx.x;
-  const long long start = tile * TILE;
-  const int cnt = (int)min((long long)TILE, p.n - start);
-  const int keep = p.keep;
-  const long long* s_key = s_col + (size_t)keep * TILE;
+constexpr int kDenseSpan = 2048;  // rows per warp span (carry unit of the fix-up)
+constexpr int kDenseThreads = 256;
 
-  const bool bulk = p.bulk_ok && cnt == TILE;
-  if (tid == 0) s_flags = 0;
-  if (bulk) {
-    if (tid == 0) {
-      mbar_init(&s_bar, 1);
-      const uint32_t col_bytes = TILE * 8u;
-      mbar_arrive_expect_tx(&s_bar, col_bytes * (p.d + 1));
-      const uint64_t pol = l2_evict_first_policy();
-      for (int m = 0; m < p.d; ++m) bulk_g2s(s_col + (size_t)m * TILE, p.col[m] + start, col_bytes, &s_bar, pol);
-      bulk_g2s(s_v, p.vals + start, col_bytes, &s_bar, pol);
-    }
-  } else {
-    for (int j = 0; j < kItems; ++j) {
-      const int r = j * 256 + tid;
-      if (r < cnt) {
-        for (int m = 0; m < p.d; ++m) s_col[m * TILE + r] = p.col[m][start + r];
-        s_v[r] = p.vals[start + r];
-      }
-    }
-  }
-  if (tid == 32) {
-    s_has_prev = start > 0;
-    s_has_next = start + cnt < p.n;
-    if (start > 0) s_prev = p.col[keep][start - 1];
-    if (start + cnt < p.n) s_next = p.col[keep][start + cnt];
-  }
-  __syncthreads();
-  if (bulk) mbar_wait(&s_bar, 0);
-
-  // w = ((vals * x_{d-1}) * x_{d-2}) ... (descending modes: the chained-TTV association)
+// Dense-result multi-vector TTV over a stream sorted by the kept mode (mode 0).
+//
+// One warp per span of kDenseSpan consecutive rows (spans handed out by an atomic ticket, the
+// next span's columns prefetched into L2 while the current one is folded).  A warp step covers
+// 128 rows as two 64-row sub-blocks; lane l holds rows 2l and 2l+1 of a sub-block (16-byte
+// loads of every column), gathers the contracted vectors for both rows (all gathers in flight
+// before the first multiply) and forms w = ((val * x_{d-1}) * ...) * x_1, the chained-TTV
+// association (descending modes).  Runs of equal keys are long (config 4: ~5000 rows), so a
+// sub-block without a head just adds into per-lane accumulators; a sub-block with a head takes
+// the slow path: the lane accumulators are reduced (butterfly), a segmented warp scan over the
+// 64 rows closes every run ending in it, and the run left open restarts the accumulators.
+// A run closed inside its span is stored straight to out[key]; the span's leading piece (before
+// its first head) and trailing open piece go to per-span carries that dense_fixup_kernel folds
+// in span order -- every output element has exactly one writer, so the result is deterministic.
+template <int D, bool V2>
+__global__ void __launch_bounds__(kDenseThreads) dense_ttv_kernel(DenseParams p, long long nspans,
+                                                                 unsigned int* ticket) {
+  const int lane = threadIdx.x & 31;
+  const int d = D > 0 ? D : p.d;
+  const long long n = p.n;
+  const unsigned long long nkeep = (unsigned long long)p.dims[0];
+  const long long* __restrict__ kcol = p.col[0];
   unsigned int flags = 0;
-  const long long nkeep = p.dims[keep];
-  // every gather of the tile in flight before the first multiply (D known at compile time)
-  double xg[D > 0 ? kItems : 1][D > 0 ? D : 1];
-  if constexpr (D > 0) {
+
+  auto grab = [&]() {
+    unsigned int t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    return (long long)__shfl_sync(0xffffffffu, t, 0);
+  };
+  auto prefetch_span = [&](long long sp) {
+    if (!V2 || sp >= nspans || lane > d) return;
+    const long long s0 = sp * kDenseSpan;
+    const uint32_t bytes = (uint32_t)(min((long long)kDenseSpan, n - s0) * 8) & ~15u;
+    const void* src = lane < d ? (const void*)(p.col[lane] + s0) : (const void*)(p.vals + s0);
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  };
+
+  long long sp = grab();
+  while (sp < nspans) {
+    const long long nxt = grab();
+    prefetch_span(nxt);
+    const long long s0 = sp * kDenseSpan;
+    const long long s1 = min(s0 + kDenseSpan, n);
+    long long curkey = s0 > 0 ? __ldg(kcol + s0 - 1) : 0;  // key of the row before the next one
+    double acc = 0.0;
+    bool seen = false;  // a head was met in this span
+    for (long long r = s0; r < s1; r += 128) {
+      long long ka[2], kb[2];
+      double wa[2], wb[2];
+      bool oka[2], okb[2];
+      constexpr int DG = D > 1 ? D : 2;  // D == 0 (any order): per-row loop below, no batching
+      long long ia[2][DG], ib[2][DG];
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const int r = j * 256 + tid;
-      const int rc = min(r, cnt - 1);
+      for (int u = 0; u < 2; ++u) {  // every column load of the step in flight at once
+        const long long a = r + 64 * u + 2 * lane;
+        oka[u] = a < s1;
+        okb[u] = a + 1 < s1;
+        if (V2 && okb[u]) {
+          const longlong2 k2 = __ldcs(reinterpret_cast<const longlong2*>(kcol + a));
+          ka[u] = k2.x, kb[u] = k2.y;
+          const double2 v2 = __ldcs(reinterpret_cast<const double2*>(p.vals + a));
+          wa[u] = v2.x, wb[u] = v2.y;
+          if constexpr (D > 0) {
 #pragma unroll
-      for (int m = 0; m < D; ++m) {
-        xg[j][m] = 1.0;
-        if (m != keep) {
-          const long long idx = s_col[m * TILE + rc];
-          const bool bad = (unsigned long long)idx >= (unsigned long long)p.dims[m];
-          if (bad && r < cnt) flags |= kFlagIndex;  // the call raises; the value is never used
-          xg[j][m] = __ldg(p.vec[m] + (bad ? 0 : idx));
+            for (int m = 1; m < D; ++m) {
+              const longlong2 i2 = __ldcs(reinterpret_cast<const longlong2*>(p.col[m] + a));
+              ia[u][m] = i2.x, ib[u][m] = i2.y;
+            }
+          }
+        } else {
+          ka[u] = oka[u] ? kcol[a] : 0;
+          kb[u] = okb[u] ? kcol[a + 1] : 0;
+          wa[u] = oka[u] ? p.vals[a] : 0.0;
+          wb[u] = okb[u] ? p.vals[a + 1] : 0.0;
+          if constexpr (D > 0) {
+#pragma unroll
+            for (int m = 1; m < D; ++m) {
+              ia[u][m] = oka[u] ? p.col[m][a] : 0;
+              ib[u][m] = okb[u] ? p.col[m][a + 1] : 0;
+            }
+          }
         }
       }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int r = j * 256 + tid;
-    bool head = false;
-    if (r < cnt) {
-      double w = s_v[r];
+      // gathers (index-checked: an out-of-range contracted index raises and is never read)
       if constexpr (D > 0) {
+        double ga[2][DG], gb[2][DG];
 #pragma unroll
-        for (int m = D - 1; m >= 0; --m)
-          if (m != keep) w = __dmul_rn(w, xg[j][m]);
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int m = 1; m < D; ++m) {
+            const unsigned long long dm = (unsigned long long)p.dims[m];
+            const bool bada = (unsigned long long)ia[u][m] >= dm, badb = (unsigned long long)ib[u][m] >= dm;
+            if ((bada && oka[u]) || (badb && okb[u])) flags |= kFlagIndex;
+            ga[u][m] = __ldg(p.vec[m] + (bada ? 0 : ia[u][m]));
+            gb[u][m] = __ldg(p.vec[m] + (badb ? 0 : ib[u][m]));
+          }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int m = D - 1; m >= 1; --m) {
+            wa[u] = __dmul_rn(wa[u], ga[u][m]);
+            wb[u] = __dmul_rn(wb[u], gb[u][m]);
+          }
       } else {
-        for (int m = p.d - 1; m >= 0; --m) {
-          if (m == keep) continue;
-          const long long idx = s_col[m * TILE + r];
-          if (idx < 0 || idx >= p.dims[m]) { flags |= kFlagIndex; w = 0.0; }
-          else w = __dmul_rn(w, __ldg(p.vec[m] + idx));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const long long a = r + 64 * u + 2 * lane;
+          for (int m = d - 1; m >= 1; --m) {
+            const unsigned long long dm = (unsigned long long)p.dims[m];
+            const long long i0 = oka[u] ? p.col[m][a] : 0, i1 = okb[u] ? p.col[m][a + 1] : 0;
+            const bool bada = (unsigned long long)i0 >= dm, badb = (unsigned long long)i1 >= dm;
+            if ((bada && oka[u]) || (badb && okb[u])) flags |= kFlagIndex;
+            wa[u] = __dmul_rn(wa[u], __ldg(p.vec[m] + (bada ? 0 : i0)));
+            wb[u] = __dmul_rn(wb[u], __ldg(p.vec[m] + (badb ? 0 : i1)));
+          }
         }
       }
-      s_v[r] = w;
-      const long long key = s_key[r];
-      if (key < 0 || key >= nkeep) flags |= kFlagKeptOob;
-      if (r == 0) head = !s_has_prev || key != s_prev, flags |= (s_has_prev && key < s_prev) ? kFlagUnsorted : 0u;
-      else {
-        const long long pk = s_key[r - 1];
-        head = key != pk;
-        if (key < pk) flags |= kFlagUnsorted;
-      }
-    }
-    const unsigned int m = __ballot_sync(0xffffffffu, head);
-    if (lane == 0) s_head[j * 8 + warp] = m;
-  }
-  if (flags) atomicOr(&s_flags, flags);
-  __syncthreads();
-
-  // blocked per-thread segmented fold
-  const int r0 = tid * kItems;
-  double first = 0.0, cur = 0.0;
-  int hh = 0;
-  long long curkey = 0;
-  for (int i = 0; i < kItems; ++i) {
-    const int r = r0 + i;
-    if (r >= cnt) break;
-    if ((s_head[r >> 5] >> (r & 31)) & 1u) {
-      if (hh) {
-        if (curkey >= 0 && curkey < nkeep) p.out[curkey] = cur;  // run wholly inside this thread
-      } else {
-        first = cur;
-        hh = 1;
-      }
-      cur = s_v[r];
-      curkey = s_key[r];
-    } else {
-      cur = (i == 0) ? s_v[r] : __dadd_rn(cur, s_v[r]);
-    }
-  }
-  // block segmented scan over threads of (has_head, last-run partial)
-  SegPair mine{hh, cur};
-  SegPair inc = mine;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    SegPair up{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-    if (lane >= o) inc = seg_combine(up, inc);
-  }
-  SegPair exc{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
-  if (lane == 0) exc = {0, 0.0};
-  if (lane == 31) s_warp[warp] = inc;
-  __syncthreads();
-  SegPair wpre{0, 0.0};
-  for (int q = 0; q < warp; ++q) wpre = seg_combine(wpre, s_warp[q]);
-  exc = lane == 0 ? wpre : seg_combine(wpre, exc);
-  inc = seg_combine(wpre, inc);
-
-  if (hh) {  // the run open at this thread's start closes at its first head
-    const double closing = __dadd_rn(exc.v, first);
-    if (exc.f) {
-      const long long k = s_key[r0 - 1];
-      if (k >= 0 && k < nkeep) p.out[k] = closing;
-    } else {
-      p.c_first[tile] = closing;
-    }
-  }
-  if (tid == 255) {
-    const long long lastkey = s_key[cnt - 1];
-    const bool last_open = s_has_next && s_next == lastkey;
-    if (inc.f) {
-      if (last_open) {
-        p.c_last[tile] = inc.v;
-        p.c_lastkey[tile] = lastkey;
-      } else if (lastkey >= 0 && lastkey < nkeep) {
-        p.out[lastkey] = inc.v;
+      for (int u = 0; u < 2; ++u) {
+        if (!oka[u]) wa[u] = 0.0;
+        if (!okb[u]) wb[u] = 0.0;
       }
-    } else {
-      p.c_first[tile] = inc.v;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const long long a = r + 64 * u + 2 * lane;
+        long long pv = __shfl_up_sync(0xffffffffu, kb[u], 1);
+        if (lane == 0) pv = curkey;
+        const bool ha = oka[u] && (ka[u] != pv || a == 0);
+        const bool hb = okb[u] && kb[u] != ka[u];
+        if ((oka[u] && a > 0 && ka[u] < pv) || (okb[u] && kb[u] < ka[u])) flags |= kFlagUnsorted;
+        if ((oka[u] && (unsigned long long)ka[u] >= nkeep) || (okb[u] && (unsigned long long)kb[u] >= nkeep))
+          flags |= kFlagKeptOob;
+        const unsigned int hm = __ballot_sync(0xffffffffu, ha || hb);
+        if (hm == 0) {
+          acc = __dadd_rn(acc, wa[u]);
+          acc = __dadd_rn(acc, wb[u]);
+        } else {
+          // slow path: close every run that ends in this sub-block
+          const double tot = warp_sum_f64(acc);
+          SegPair inc{ha || hb, hb ? wb[u] : __dadd_rn(wa[u], wb[u])};
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const SegPair up{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+            if (lane >= o) inc = seg_combine(up, inc);
+          }
+          SegPair exc{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
+          if (lane == 0) exc = {0, 0.0};
+          // a head at row h closes the run ending at h-1 (continuing the open run when no head
+          // precedes h in the sub-block); the open run's first closing before any head of the
+          // span is the span's leading carry
+          auto close = [&](bool cont, long long key, double v) {
+            if (cont && !seen) p.c_first[sp] = v;
+            else if ((unsigned long long)key < nkeep) p.out[key] = v;
+          };
+          if (ha) close(!exc.f, pv, exc.f ? exc.v : __dadd_rn(tot, exc.v));
+          if (hb) {
+            const int fa = exc.f | (int)ha;
+            const double va = ha ? wa[u] : __dadd_rn(exc.v, wa[u]);
+            close(!fa, ka[u], fa ? va : __dadd_rn(tot, va));
+          }
+          const double open = __shfl_sync(0xffffffffu, inc.v, 31);
+          acc = lane == 0 ? open : 0.0;
+          seen = true;
+        }
+        // key of the last valid row of the sub-block
+        const unsigned int mb = __ballot_sync(0xffffffffu, okb[u]), ma = __ballot_sync(0xffffffffu, oka[u]);
+        if (mb == 0xffffffffu) {
+          curkey = __shfl_sync(0xffffffffu, kb[u], 31);
+        } else if (ma) {
+          const int la = 31 - __clz(ma), lb = mb ? 31 - __clz(mb) : -1;
+          const long long kla = __shfl_sync(0xffffffffu, ka[u], la);
+          const long long klb = __shfl_sync(0xffffffffu, kb[u], lb < 0 ? 0 : lb);
+          curkey = la > lb ? kla : klb;
+        }
+      }
     }
-    p.c_flags[tile] = (inc.f ? 1 : 0) | (last_open ? 2 : 0);
-    if (s_flags) atomicOr(&p.ctr->flags, s_flags);
+    const double total = warp_sum_f64(acc);
+    if (lane == 0) {
+      const bool last_open = s1 < n && __ldg(kcol + s1) == curkey;
+      if (!seen) {
+        p.c_first[sp] = total;
+      } else if (last_open) {
+        p.c_last[sp] = total;
+        p.c_lastkey[sp] = curkey;
+      } else if ((unsigned long long)curkey < nkeep) {
+        p.out[curkey] = total;
+      }
+      p.c_flags[sp] = (seen ? 1 : 0) | (last_open ? 2 : 0);
+    }
+    sp = nxt;
   }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lane == 0 && flags) atomicOr(&p.ctr->flags, flags);
 }
 
 __global__ void dense_fixup_kernel(long long ntiles, const double* __restrict__ c_first,
@@ -722,11 +755,10 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
   TK_CUDA(cudaMemsetAsync(out, 0, (size_t)nkeep * 8, st));
   if (nnz == 0) return TK_OK;
   Counters* hc = static_cast<Counters*>(pinned_scratch(sizeof(Counters)));
-  if (keep == 0) {
-    constexpr int kItems = 4, TILE = kItems * 256;
-    const long long ntiles = (nnz + TILE - 1) / TILE;
+  if (keep == 0 && d >= 2) {
+    const long long nspans = (nnz + kDenseSpan - 1) / kDenseSpan;
     DevBuf scratch;
-    const size_t per = (size_t)ntiles * 8;
+    const size_t per = ((size_t)nspans * 8 + 255) & ~size_t(255);
     if (int rc = scratch.alloc(per * 4 + 512, st)) return rc;
     DenseParams p{};
     p.n = nnz;
@@ -746,19 +778,42 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     p.c_last = reinterpret_cast<double*>(b + per);
     p.c_lastkey = reinterpret_cast<long long*>(b + 2 * per);
     p.c_flags = reinterpret_cast<int*>(b + 3 * per);
-    p.ctr = reinterpret_cast<Counters*>(b + 4 * per + 128);
+    p.ctr = reinterpret_cast<Counters*>(b + 4 * per);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(b + 4 * per + 256);
     p.bulk_ok = al;
-    TK_CUDA(cudaMemsetAsync(p.ctr, 0, sizeof(Counters), st));
-    const size_t smem = (size_t)(d + 1) * TILE * 8;
-    auto kern = d == 3 ? dense_ttv_kernel<kItems, 3> : d == 4 ? dense_ttv_kernel<kItems, 4>
-                : d == 5 ? dense_ttv_kernel<kItems, 5> : dense_ttv_kernel<kItems, 0>;
-    set_smem_once(kern, smem);
+    TK_CUDA(cudaMemsetAsync(b + 4 * per, 0, 512, st));
+    using K = void (*)(DenseParams, long long, unsigned int*);
+    K kern;
+    switch (d) {
+      case 2: kern = al ? dense_ttv_kernel<2, true> : dense_ttv_kernel<2, false>; break;
+      case 3: kern = al ? dense_ttv_kernel<3, true> : dense_ttv_kernel<3, false>; break;
+      case 4: kern = al ? dense_ttv_kernel<4, true> : dense_ttv_kernel<4, false>; break;
+      case 5: kern = al ? dense_ttv_kernel<5, true> : dense_ttv_kernel<5, false>; break;
+      default: kern = al ? dense_ttv_kernel<0, true> : dense_ttv_kernel<0, false>; break;
+    }
+    // resident CTAs per SM of the chosen instance (looked up once per instance and device)
+    static std::mutex occ_mu;
+    static std::map<std::pair<const void*, int>, int> occ_cache;
+    int dev = 0, occ = 0;
+    TK_CUDA(cudaGetDevice(&dev));
+    {
+      std::lock_guard<std::mutex> lk(occ_mu);
+      int& o = occ_cache[{reinterpret_cast<const void*>(kern), dev}];
+      if (!o) {
+        TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kDenseThreads, 0));
+        o = std::max(o, 1);
+      }
+      occ = o;
+    }
+    const long long wpb = kDenseThreads / 32;
+    const long long warps = std::min(nspans, (long long)num_sms() * occ * wpb);
+    const long long blocks = (warps + wpb - 1) / wpb;
     ktimer_begin(st);
-    kern<<<(unsigned)ntiles, 256, smem, st>>>(p);
+    kern<<<(unsigned)blocks, kDenseThreads, 0, st>>>(p, nspans, ticket);
     ktimer_end(st);
     count_launch(2);
-    dense_fixup_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(ntiles, p.c_first, p.c_last, p.c_lastkey,
-                                                                         p.c_flags, nkeep, out);
+    dense_fixup_kernel<<<(unsigned)((nspans + 255) / 256), 256, 0, st>>>(nspans, p.c_first, p.c_last, p.c_lastkey,
+                                                                         p.c_flags, shape[0], out);
     TK_CUDA(cudaGetLastError());
     TK_CUDA(cudaMemcpyAsync(hc, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     TK_CUDA(cudaStreamSynchronize(st));

@@ -354,3 +354,72 @@ def test_host_pipeline_declines_unsorted_and_reports_index_errors():
     bad[-5, 2] = shape[2]
     with pytest.raises(errors.DimensionError):
         _host_ttv(bad, vals, shape, x.cpu().numpy(), 2)
+
+
+def _canonical_coo(shape, nnz, seed):
+    """Distinct uniform coordinates in canonical (lexicographic) order, positive values."""
+    rng = np.random.default_rng(seed)
+    total = int(np.prod(np.asarray(shape, dtype=np.float64)))
+    lin = np.unique(rng.integers(0, total, size=nnz, dtype=np.int64))
+    subs = np.stack(np.unravel_index(lin, shape), axis=1).astype(np.int64)
+    vals = rng.random(len(lin)) + 0.5
+    return np.ascontiguousarray(subs), vals
+
+
+@pytest.mark.parametrize("shape,nnz", [
+    ((5000, 3, 3, 3), 20000),        # runs of ~4 rows: several heads in most 64-row sub-blocks
+    ((300, 40, 50), 700000),         # runs of ~2300 rows: cross the 2048-row span boundaries
+    ((1, 700, 800), 150000),         # one run over ~73 spans
+    ((64, 100), 3000),               # order 2 (a dense matvec-like contraction)
+    ((40, 6, 7, 8, 9), 50000),       # order 5
+    ((9, 4, 4, 4, 4, 4), 20000),     # order 6: the any-order instance
+    ((1000, 10, 10, 10), 1),         # a single row
+    ((50, 20, 20, 20), 2049),        # odd row count just past one span
+])
+def test_dense_kernel_edge_cases(oracle, shape, nnz):
+    """Dense multi-vector kernel (keep = 0): short and long runs, span-crossing runs, orders
+    2-6, odd and tiny row counts, gaps in the kept mode; within 1e-12 of the chained oracle."""
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo
+    subs, vals = _canonical_coo(shape, nnz, seed=sum(shape) + nnz)
+    t = DeviceCoo.from_host(subs, vals, shape)
+    rng = np.random.default_rng(nnz)
+    hv = {m: rng.random(shape[m]) + 0.5 for m in range(1, len(shape))}
+    vecs = {m: torch.from_numpy(v).cuda() for m, v in hv.items()}
+    out = t.ttv_dense(vecs, 0).cpu().numpy()
+    ref = oracle.ttv_multi_dense(subs, vals, shape, hv, 0)
+    assert np.array_equal(out != 0, ref != 0)
+    nz = ref != 0
+    assert np.max(np.abs(out[nz] - ref[nz]) / np.abs(ref[nz]), initial=0.0) <= REL
+    # deterministic run to run
+    assert t.ttv_dense(vecs, 0).cpu().numpy().tobytes() == out.tobytes()
+    # 8-byte-aligned (not 16) columns: the scalar-load instance gives the same bits
+    if t.nnz > 1:
+        u = t.slice(1, t.nnz, copy=False)
+        s1, v1 = subs[1:], vals[1:]
+        o1 = u.ttv_dense(vecs, 0).cpu().numpy()
+        r1 = oracle.ttv_multi_dense(s1, v1, shape, hv, 0)
+        nz1 = r1 != 0
+        assert np.array_equal(o1 != 0, nz1)
+        assert np.max(np.abs(o1[nz1] - r1[nz1]) / np.abs(r1[nz1]), initial=0.0) <= REL
+
+
+def test_dense_kernel_errors_and_unsorted(oracle):
+    """Contracted index out of range raises DimensionError; an unsorted kept mode is detected
+    and the chained path gives the (bit-exact) chained-oracle result."""
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo
+    from paper_2510_01495_b200.errors import DimensionError
+    shape = (30, 20, 20, 20)
+    subs, vals = _canonical_coo(shape, 5000, seed=9)
+    hv = {m: np.random.default_rng(m).random(shape[m]) + 0.5 for m in (1, 2, 3)}
+    vecs = {m: torch.from_numpy(v).cuda() for m, v in hv.items()}
+    bad = subs.copy()
+    bad[1234, 2] = 20
+    with pytest.raises(DimensionError):
+        DeviceCoo.from_host(bad, vals, shape).ttv_dense(vecs, 0)
+    perm = np.random.default_rng(3).permutation(len(vals))
+    t = DeviceCoo.from_host(subs[perm], vals[perm], shape)
+    out = t.ttv_dense(vecs, 0).cpu().numpy()
+    ref = oracle.ttv_multi_dense(subs[perm], vals[perm], shape, hv, 0)
+    assert out.tobytes() == ref.tobytes()
