@@ -188,199 +188,302 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;  // identical in every lane (RN addition commutes)
 }
 
-constexpr int kDenseSpan = 2048;  // rows per warp span (carry unit of the fix-up)
+#ifndef TK_DENSE_SPAN
+#define TK_DENSE_SPAN 2048
+#endif
+#ifndef TK_DENSE_U
+#define TK_DENSE_U 1
+#endif
+#ifndef TK_DENSE_MINB
+#define TK_DENSE_MINB 2
+#endif
+constexpr int kDenseSpan = TK_DENSE_SPAN;  // rows per warp span (carry unit of the fix-up)
 constexpr int kDenseThreads = 256;
+#ifndef TK_DENSE_SV_THREADS
+#define TK_DENSE_SV_THREADS 512
+#endif
+#ifndef TK_DENSE_SV_MAX
+#define TK_DENSE_SV_MAX (192 * 1024)  // largest staged vector (bytes); the rest of L1 caches the others
+#endif
+constexpr int kDenseSvThreads = TK_DENSE_SV_THREADS;
+constexpr int kDenseU = TK_DENSE_U;        // 64-row sub-blocks per warp step
 
 // Dense-result multi-vector TTV over a stream sorted by the kept mode (mode 0).
 //
-// One warp per span of kDenseSpan consecutive rows (spans handed out by an atomic ticket, the
-// next span's columns prefetched into L2 while the current one is folded).  A warp step covers
-// 128 rows as two 64-row sub-blocks; lane l holds rows 2l and 2l+1 of a sub-block (16-byte
-// loads of every column), gathers the contracted vectors for both rows (all gathers in flight
-// before the first multiply) and forms w = ((val * x_{d-1}) * ...) * x_1, the chained-TTV
-// association (descending modes).  Runs of equal keys are long (config 4: ~5000 rows), so a
-// sub-block without a head just adds into per-lane accumulators; a sub-block with a head takes
-// the slow path: the lane accumulators are reduced (butterfly), a segmented warp scan over the
-// 64 rows closes every run ending in it, and the run left open restarts the accumulators.
-// A run closed inside its span is stored straight to out[key]; the span's leading piece (before
-// its first head) and trailing open piece go to per-span carries that dense_fixup_kernel folds
-// in span order -- every output element has exactly one writer, so the result is deterministic.
-template <int D, bool V2>
-__global__ void __launch_bounds__(kDenseThreads) dense_ttv_kernel(DenseParams p, long long nspans,
-                                                                 unsigned int* ticket) {
+// One warp per span of kDenseSpan consecutive rows.  A warp step covers 64*kDenseU rows as
+// 64-row sub-blocks; lane l holds rows 2l and 2l+1 of a sub-block (16-byte loads of every
+// column), gathers the contracted vectors for both rows and forms
+// w = ((val * x_{d-1}) * ...) * x_1, the chained-TTV association (descending modes).  Runs of
+// equal keys are long (config 4: ~5000 rows), so a sub-block without a head just adds into
+// per-lane accumulators; a sub-block with a head takes the slow path: the lane accumulators are
+// reduced (butterfly), a segmented warp scan over the 64 rows closes every run ending in it, and
+// the run left open restarts the accumulators.  A run closed inside its span is stored straight
+// to out[key]; the span's leading piece (before its first head) and trailing open piece go to
+// per-span carries that dense_fixup_kernel folds in span order -- every output element has
+// exactly one writer, so the result is deterministic.
+template <int D, int U>
+struct DenseStep {
+  static constexpr int DG = D > 1 ? D : 2;  // D == 0 (any order): indices re-read per row, no batching
+  long long ka[U], kb[U];
+  double wa[U], wb[U];
+  long long ia[U][DG], ib[U][DG];
+  bool oka[U], okb[U];
+};
+
+template <int D, bool V2, int U>
+__device__ __forceinline__ void dense_load_step(const DenseParams& p, long long r, long long s1,
+                                                DenseStep<D, U>& s) {
+  const int lane = threadIdx.x & 31;
+  const long long* __restrict__ kcol = p.col[0];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {  // every column load of the step in flight at once
+    const long long a = r + 64 * u + 2 * lane;
+    s.oka[u] = a < s1;
+    s.okb[u] = a + 1 < s1;
+    if (V2 && s.okb[u]) {
+      const longlong2 k2 = __ldcs(reinterpret_cast<const longlong2*>(kcol + a));
+      s.ka[u] = k2.x, s.kb[u] = k2.y;
+      const double2 v2 = __ldcs(reinterpret_cast<const double2*>(p.vals + a));
+      s.wa[u] = v2.x, s.wb[u] = v2.y;
+      if constexpr (D > 0) {
+#pragma unroll
+        for (int m = 1; m < D; ++m) {
+          const longlong2 i2 = __ldcs(reinterpret_cast<const longlong2*>(p.col[m] + a));
+          s.ia[u][m] = i2.x, s.ib[u][m] = i2.y;
+        }
+      }
+    } else {
+      s.ka[u] = s.oka[u] ? kcol[a] : 0;
+      s.kb[u] = s.okb[u] ? kcol[a + 1] : 0;
+      s.wa[u] = s.oka[u] ? p.vals[a] : 0.0;
+      s.wb[u] = s.okb[u] ? p.vals[a + 1] : 0.0;
+      if constexpr (D > 0) {
+#pragma unroll
+        for (int m = 1; m < D; ++m) {
+          s.ia[u][m] = s.oka[u] ? p.col[m][a] : 0;
+          s.ib[u][m] = s.okb[u] ? p.col[m][a + 1] : 0;
+        }
+      }
+    }
+  }
+}
+
+// Gathered contracted-vector entries of one step (rows 2l, 2l+1 of every sub-block).
+template <int D, int U>
+struct DenseGath {
+  static constexpr int DG = D > 1 ? D : 2;
+  double ga[U][DG], gb[U][DG];
+};
+
+// Issue the gathers of a loaded step (index-checked: an out-of-range contracted index raises
+// and is never read).  SV: the last mode's vector is read from shared memory.
+template <int D, int U, bool SV>
+__device__ __forceinline__ void dense_gather_step(const DenseParams& p, const DenseStep<D, U>& s,
+                                                  const double* s_vec, DenseGath<D, U>& g, unsigned int& flags) {
+  if constexpr (D > 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 1; m < D; ++m) {
+        const unsigned long long dm = (unsigned long long)p.dims[m];
+        const bool bada = (unsigned long long)s.ia[u][m] >= dm, badb = (unsigned long long)s.ib[u][m] >= dm;
+        if ((bada && s.oka[u]) || (badb && s.okb[u])) flags |= kFlagIndex;
+#ifdef TK_DENSE_NOGATHER  // A/B experiment only: stream without gathers (wrong results)
+        g.ga[u][m] = (double)(s.ia[u][m] & 7);
+        g.gb[u][m] = (double)(s.ib[u][m] & 7);
+        continue;
+#endif
+        if (SV && m == D - 1) {
+          g.ga[u][m] = s_vec[bada ? 0 : s.ia[u][m]];
+          g.gb[u][m] = s_vec[badb ? 0 : s.ib[u][m]];
+        } else {
+          g.ga[u][m] = __ldg(p.vec[m] + (bada ? 0 : s.ia[u][m]));
+          g.gb[u][m] = __ldg(p.vec[m] + (badb ? 0 : s.ib[u][m]));
+        }
+      }
+  }
+}
+
+// SV (staged vector): the last mode's vector is copied into shared memory once per CTA (one
+// persistent CTA of kDenseSvThreads per SM), so its random gathers are LDS instead of L1/L2
+// requests.
+//
+// Three-stage software pipeline per warp over its static sequence of spans (warp w takes spans
+// w, w+W, w+2W, ...; W = warps in the grid): while step i is folded, the gathers of step i+1 and
+// the column loads of step i+2 are in flight, so neither the stream nor the gathers wait on the
+// fold's dependency chain.
+template <int D, bool V2, bool SV>
+__global__ void __launch_bounds__(SV ? kDenseSvThreads : kDenseThreads, SV ? 1 : TK_DENSE_MINB)
+    dense_ttv_kernel(DenseParams p, long long nspans) {
+  constexpr int U = kDenseU;
+  constexpr long long STEP = 64 * U;
+  extern __shared__ __align__(16) double s_vec[];
+  if constexpr (SV) {
+    // every load of the copy in flight at once (a serial loop of L2 round trips would cost
+    // tens of microseconds per CTA)
+    const long long nv = p.dims[D - 1];
+    const double* __restrict__ g = p.vec[D - 1];
+    constexpr int R = 8;
+    for (long long i0 = 0; i0 < nv; i0 += (long long)R * blockDim.x) {
+      double v[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const long long i = i0 + (long long)j * blockDim.x + threadIdx.x;
+        v[j] = i < nv ? __ldg(g + i) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const long long i = i0 + (long long)j * blockDim.x + threadIdx.x;
+        if (i < nv) s_vec[i] = v[j];
+      }
+    }
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int d = D > 0 ? D : p.d;
   const long long n = p.n;
   const unsigned long long nkeep = (unsigned long long)p.dims[0];
   const long long* __restrict__ kcol = p.col[0];
+  const long long W = ((long long)gridDim.x * blockDim.x) >> 5;
   unsigned int flags = 0;
 
-  auto grab = [&]() {
-    unsigned int t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1u);
-    return (long long)__shfl_sync(0xffffffffu, t, 0);
-  };
-  auto prefetch_span = [&](long long sp) {
-    if (!V2 || sp >= nspans || lane > d) return;
-    const long long s0 = sp * kDenseSpan;
-    const uint32_t bytes = (uint32_t)(min((long long)kDenseSpan, n - s0) * 8) & ~15u;
-    const void* src = lane < d ? (const void*)(p.col[lane] + s0) : (const void*)(p.vals + s0);
-    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  auto span_end = [&](long long sp) { return min((sp + 1) * kDenseSpan, n); };
+  // step cursor over the warp's span sequence
+  auto advance = [&](long long& sp, long long& r) {
+    r += STEP;
+    if (r >= span_end(sp)) {
+      sp += W;
+      r = sp * kDenseSpan;
+    }
   };
 
-  long long sp = grab();
-  while (sp < nspans) {
-    const long long nxt = grab();
-    prefetch_span(nxt);
-    const long long s0 = sp * kDenseSpan;
-    const long long s1 = min(s0 + kDenseSpan, n);
-    long long curkey = s0 > 0 ? __ldg(kcol + s0 - 1) : 0;  // key of the row before the next one
-    double acc = 0.0;
-    bool seen = false;  // a head was met in this span
-    for (long long r = s0; r < s1; r += 128) {
-      long long ka[2], kb[2];
-      double wa[2], wb[2];
-      bool oka[2], okb[2];
-      constexpr int DG = D > 1 ? D : 2;  // D == 0 (any order): per-row loop below, no batching
-      long long ia[2][DG], ib[2][DG];
+  long long fsp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // fold cursor
+  if (fsp >= nspans) return;
+  long long fr = fsp * kDenseSpan;
+  long long gsp = fsp, gr = fr;  // gather cursor (one step ahead)
+  advance(gsp, gr);
+  long long lsp = gsp, lr = gr;  // load cursor (two steps ahead)
+  advance(lsp, lr);
+
+  DenseStep<D, U> cs, gs, ls;  // steps at the fold, gather and load cursors
+  DenseGath<D, U> cg, gg;      // gathered entries of the fold / gather steps
+  dense_load_step<D, V2, U>(p, fr, span_end(fsp), cs);
+  if (gsp < nspans) dense_load_step<D, V2, U>(p, gr, span_end(gsp), gs);
+  dense_gather_step<D, U, SV>(p, cs, s_vec, cg, flags);
+
+  long long curkey = fsp > 0 ? __ldg(kcol + fr - 1) : 0;  // key of the row before the next one
+  double acc = 0.0;
+  bool seen = false;  // a head was met in this span
+  while (true) {
+    if (lsp < nspans) dense_load_step<D, V2, U>(p, lr, span_end(lsp), ls);
+    if (gsp < nspans) dense_gather_step<D, U, SV>(p, gs, s_vec, gg, flags);
+
+    // ---- fold the step at (fsp, fr) ----
+    const long long r = fr;
+    const long long s1 = span_end(fsp);
+    if constexpr (D > 0) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {  // every column load of the step in flight at once
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int m = D - 1; m >= 1; --m) {
+          cs.wa[u] = __dmul_rn(cs.wa[u], cg.ga[u][m]);
+          cs.wb[u] = __dmul_rn(cs.wb[u], cg.gb[u][m]);
+        }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const long long a = r + 64 * u + 2 * lane;
-        oka[u] = a < s1;
-        okb[u] = a + 1 < s1;
-        if (V2 && okb[u]) {
-          const longlong2 k2 = __ldcs(reinterpret_cast<const longlong2*>(kcol + a));
-          ka[u] = k2.x, kb[u] = k2.y;
-          const double2 v2 = __ldcs(reinterpret_cast<const double2*>(p.vals + a));
-          wa[u] = v2.x, wb[u] = v2.y;
-          if constexpr (D > 0) {
-#pragma unroll
-            for (int m = 1; m < D; ++m) {
-              const longlong2 i2 = __ldcs(reinterpret_cast<const longlong2*>(p.col[m] + a));
-              ia[u][m] = i2.x, ib[u][m] = i2.y;
-            }
-          }
-        } else {
-          ka[u] = oka[u] ? kcol[a] : 0;
-          kb[u] = okb[u] ? kcol[a + 1] : 0;
-          wa[u] = oka[u] ? p.vals[a] : 0.0;
-          wb[u] = okb[u] ? p.vals[a + 1] : 0.0;
-          if constexpr (D > 0) {
-#pragma unroll
-            for (int m = 1; m < D; ++m) {
-              ia[u][m] = oka[u] ? p.col[m][a] : 0;
-              ib[u][m] = okb[u] ? p.col[m][a + 1] : 0;
-            }
-          }
+        for (int m = d - 1; m >= 1; --m) {
+          const unsigned long long dm = (unsigned long long)p.dims[m];
+          const long long i0 = cs.oka[u] ? p.col[m][a] : 0, i1 = cs.okb[u] ? p.col[m][a + 1] : 0;
+          const bool bada = (unsigned long long)i0 >= dm, badb = (unsigned long long)i1 >= dm;
+          if ((bada && cs.oka[u]) || (badb && cs.okb[u])) flags |= kFlagIndex;
+          cs.wa[u] = __dmul_rn(cs.wa[u], __ldg(p.vec[m] + (bada ? 0 : i0)));
+          cs.wb[u] = __dmul_rn(cs.wb[u], __ldg(p.vec[m] + (badb ? 0 : i1)));
         }
       }
-      // gathers (index-checked: an out-of-range contracted index raises and is never read)
-      if constexpr (D > 0) {
-        double ga[2][DG], gb[2][DG];
+    }
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int m = 1; m < D; ++m) {
-            const unsigned long long dm = (unsigned long long)p.dims[m];
-            const bool bada = (unsigned long long)ia[u][m] >= dm, badb = (unsigned long long)ib[u][m] >= dm;
-            if ((bada && oka[u]) || (badb && okb[u])) flags |= kFlagIndex;
-            ga[u][m] = __ldg(p.vec[m] + (bada ? 0 : ia[u][m]));
-            gb[u][m] = __ldg(p.vec[m] + (badb ? 0 : ib[u][m]));
-          }
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int m = D - 1; m >= 1; --m) {
-            wa[u] = __dmul_rn(wa[u], ga[u][m]);
-            wb[u] = __dmul_rn(wb[u], gb[u][m]);
-          }
+    for (int u = 0; u < U; ++u) {
+      const long long a = r + 64 * u + 2 * lane;
+      const long long ka = cs.ka[u], kb = cs.kb[u];
+      const bool oka = cs.oka[u], okb = cs.okb[u];
+      const double wa = oka ? cs.wa[u] : 0.0, wb = okb ? cs.wb[u] : 0.0;
+      long long pv = __shfl_up_sync(0xffffffffu, kb, 1);
+      if (lane == 0) pv = curkey;
+      const bool ha = oka && (ka != pv || a == 0);
+      const bool hb = okb && kb != ka;
+      if ((oka && a > 0 && ka < pv) || (okb && kb < ka)) flags |= kFlagUnsorted;
+      if ((oka && (unsigned long long)ka >= nkeep) || (okb && (unsigned long long)kb >= nkeep)) flags |= kFlagKeptOob;
+      const unsigned int hm = __ballot_sync(0xffffffffu, ha || hb);
+      if (hm == 0) {
+        acc = __dadd_rn(acc, wa);
+        acc = __dadd_rn(acc, wb);
       } else {
+        // slow path: close every run that ends in this sub-block
+        const double tot = warp_sum_f64(acc);
+        SegPair inc{ha || hb, hb ? wb : __dadd_rn(wa, wb)};
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const long long a = r + 64 * u + 2 * lane;
-          for (int m = d - 1; m >= 1; --m) {
-            const unsigned long long dm = (unsigned long long)p.dims[m];
-            const long long i0 = oka[u] ? p.col[m][a] : 0, i1 = okb[u] ? p.col[m][a + 1] : 0;
-            const bool bada = (unsigned long long)i0 >= dm, badb = (unsigned long long)i1 >= dm;
-            if ((bada && oka[u]) || (badb && okb[u])) flags |= kFlagIndex;
-            wa[u] = __dmul_rn(wa[u], __ldg(p.vec[m] + (bada ? 0 : i0)));
-            wb[u] = __dmul_rn(wb[u], __ldg(p.vec[m] + (badb ? 0 : i1)));
-          }
+        for (int o = 1; o < 32; o <<= 1) {
+          const SegPair up{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+          if (lane >= o) inc = seg_combine(up, inc);
         }
+        SegPair exc{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
+        if (lane == 0) exc = {0, 0.0};
+        // a head at row h closes the run ending at h-1 (continuing the open run when no head
+        // precedes h in the sub-block); the open run's first closing before any head of the
+        // span is the span's leading carry
+        auto close = [&](bool cont, long long key, double v) {
+          if (cont && !seen) p.c_first[fsp] = v;
+          else if ((unsigned long long)key < nkeep) p.out[key] = v;
+        };
+        if (ha) close(!exc.f, pv, exc.f ? exc.v : __dadd_rn(tot, exc.v));
+        if (hb) {
+          const int fa = exc.f | (int)ha;
+          const double va = ha ? wa : __dadd_rn(exc.v, wa);
+          close(!fa, ka, fa ? va : __dadd_rn(tot, va));
+        }
+        const double open = __shfl_sync(0xffffffffu, inc.v, 31);
+        acc = lane == 0 ? open : 0.0;
+        seen = true;
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!oka[u]) wa[u] = 0.0;
-        if (!okb[u]) wb[u] = 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const long long a = r + 64 * u + 2 * lane;
-        long long pv = __shfl_up_sync(0xffffffffu, kb[u], 1);
-        if (lane == 0) pv = curkey;
-        const bool ha = oka[u] && (ka[u] != pv || a == 0);
-        const bool hb = okb[u] && kb[u] != ka[u];
-        if ((oka[u] && a > 0 && ka[u] < pv) || (okb[u] && kb[u] < ka[u])) flags |= kFlagUnsorted;
-        if ((oka[u] && (unsigned long long)ka[u] >= nkeep) || (okb[u] && (unsigned long long)kb[u] >= nkeep))
-          flags |= kFlagKeptOob;
-        const unsigned int hm = __ballot_sync(0xffffffffu, ha || hb);
-        if (hm == 0) {
-          acc = __dadd_rn(acc, wa[u]);
-          acc = __dadd_rn(acc, wb[u]);
-        } else {
-          // slow path: close every run that ends in this sub-block
-          const double tot = warp_sum_f64(acc);
-          SegPair inc{ha || hb, hb ? wb[u] : __dadd_rn(wa[u], wb[u])};
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const SegPair up{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-            if (lane >= o) inc = seg_combine(up, inc);
-          }
-          SegPair exc{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
-          if (lane == 0) exc = {0, 0.0};
-          // a head at row h closes the run ending at h-1 (continuing the open run when no head
-          // precedes h in the sub-block); the open run's first closing before any head of the
-          // span is the span's leading carry
-          auto close = [&](bool cont, long long key, double v) {
-            if (cont && !seen) p.c_first[sp] = v;
-            else if ((unsigned long long)key < nkeep) p.out[key] = v;
-          };
-          if (ha) close(!exc.f, pv, exc.f ? exc.v : __dadd_rn(tot, exc.v));
-          if (hb) {
-            const int fa = exc.f | (int)ha;
-            const double va = ha ? wa[u] : __dadd_rn(exc.v, wa[u]);
-            close(!fa, ka[u], fa ? va : __dadd_rn(tot, va));
-          }
-          const double open = __shfl_sync(0xffffffffu, inc.v, 31);
-          acc = lane == 0 ? open : 0.0;
-          seen = true;
-        }
-        // key of the last valid row of the sub-block
-        const unsigned int mb = __ballot_sync(0xffffffffu, okb[u]), ma = __ballot_sync(0xffffffffu, oka[u]);
-        if (mb == 0xffffffffu) {
-          curkey = __shfl_sync(0xffffffffu, kb[u], 31);
-        } else if (ma) {
-          const int la = 31 - __clz(ma), lb = mb ? 31 - __clz(mb) : -1;
-          const long long kla = __shfl_sync(0xffffffffu, ka[u], la);
-          const long long klb = __shfl_sync(0xffffffffu, kb[u], lb < 0 ? 0 : lb);
-          curkey = la > lb ? kla : klb;
-        }
+      // key of the last valid row of the sub-block
+      const unsigned int mb = __ballot_sync(0xffffffffu, okb), ma = __ballot_sync(0xffffffffu, oka);
+      if (mb == 0xffffffffu) {
+        curkey = __shfl_sync(0xffffffffu, kb, 31);
+      } else if (ma) {
+        const int la = 31 - __clz(ma), lb = mb ? 31 - __clz(mb) : -1;
+        const long long kla = __shfl_sync(0xffffffffu, ka, la);
+        const long long klb = __shfl_sync(0xffffffffu, kb, lb < 0 ? 0 : lb);
+        curkey = la > lb ? kla : klb;
       }
     }
-    const double total = warp_sum_f64(acc);
-    if (lane == 0) {
-      const bool last_open = s1 < n && __ldg(kcol + s1) == curkey;
-      if (!seen) {
-        p.c_first[sp] = total;
-      } else if (last_open) {
-        p.c_last[sp] = total;
-        p.c_lastkey[sp] = curkey;
-      } else if ((unsigned long long)curkey < nkeep) {
-        p.out[curkey] = total;
+    if (r + STEP >= s1) {  // span finished: its carries
+      const double total = warp_sum_f64(acc);
+      if (lane == 0) {
+        const bool last_open = s1 < n && __ldg(kcol + s1) == curkey;
+        if (!seen) {
+          p.c_first[fsp] = total;
+        } else if (last_open) {
+          p.c_last[fsp] = total;
+          p.c_lastkey[fsp] = curkey;
+        } else if ((unsigned long long)curkey < nkeep) {
+          p.out[curkey] = total;
+        }
+        p.c_flags[fsp] = (seen ? 1 : 0) | (last_open ? 2 : 0);
       }
-      p.c_flags[sp] = (seen ? 1 : 0) | (last_open ? 2 : 0);
+      if (gsp >= nspans) break;
+      curkey = __ldg(kcol + gsp * kDenseSpan - 1);  // gsp > fsp >= 0
+      acc = 0.0;
+      seen = false;
     }
-    sp = nxt;
+    // rotate the pipeline
+    fsp = gsp, fr = gr;
+    gsp = lsp, gr = lr;
+    advance(lsp, lr);
+    cs = gs;
+    cg = gg;
+    gs = ls;
   }
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (lane == 0 && flags) atomicOr(&p.ctr->flags, flags);
@@ -408,8 +511,10 @@ __global__ void dense_fixup_kernel(long long ntiles, const double* __restrict__ 
 namespace {
 
 // Opt a kernel in to >48 KB of dynamic shared memory, once per (kernel, device).
+// carveout: preferred shared-memory share of the unified L1 (percent); the tile kernels take it
+// all, the staged-vector dense kernel only what its vector needs (L1 caches the other vectors).
 template <class K>
-void set_smem_once(K kernel, size_t bytes) {
+void set_smem_once(K kernel, size_t bytes, int carveout = 100) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> done;
   int dev = 0;
@@ -418,8 +523,7 @@ void set_smem_once(K kernel, size_t bytes) {
   size_t& have = done[{reinterpret_cast<const void*>(kernel), dev}];
   if (bytes > have) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    // all shared memory: eight tile CTAs need ~216 KB; x's hot entries still fit the rest of L1
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     have = bytes;
   }
 }
@@ -779,18 +883,26 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     p.c_lastkey = reinterpret_cast<long long*>(b + 2 * per);
     p.c_flags = reinterpret_cast<int*>(b + 3 * per);
     p.ctr = reinterpret_cast<Counters*>(b + 4 * per);
-    unsigned int* ticket = reinterpret_cast<unsigned int*>(b + 4 * per + 256);
     p.bulk_ok = al;
     TK_CUDA(cudaMemsetAsync(b + 4 * per, 0, 512, st));
-    using K = void (*)(DenseParams, long long, unsigned int*);
+    using K = void (*)(DenseParams, long long);
+    const size_t sv_bytes = (size_t)shape[d - 1] * 8;
+    const bool sv = d >= 3 && d <= 5 && sv_bytes <= TK_DENSE_SV_MAX;
     K kern;
+#define TK_DENSE_PICK(DD) \
+  kern = sv ? (al ? dense_ttv_kernel<DD, true, true> : dense_ttv_kernel<DD, false, true>) \
+            : (al ? dense_ttv_kernel<DD, true, false> : dense_ttv_kernel<DD, false, false>)
     switch (d) {
-      case 2: kern = al ? dense_ttv_kernel<2, true> : dense_ttv_kernel<2, false>; break;
-      case 3: kern = al ? dense_ttv_kernel<3, true> : dense_ttv_kernel<3, false>; break;
-      case 4: kern = al ? dense_ttv_kernel<4, true> : dense_ttv_kernel<4, false>; break;
-      case 5: kern = al ? dense_ttv_kernel<5, true> : dense_ttv_kernel<5, false>; break;
-      default: kern = al ? dense_ttv_kernel<0, true> : dense_ttv_kernel<0, false>; break;
+      case 2: kern = al ? dense_ttv_kernel<2, true, false> : dense_ttv_kernel<2, false, false>; break;
+      case 3: TK_DENSE_PICK(3); break;
+      case 4: TK_DENSE_PICK(4); break;
+      case 5: TK_DENSE_PICK(5); break;
+      default: kern = al ? dense_ttv_kernel<0, true, false> : dense_ttv_kernel<0, false, false>; break;
     }
+#undef TK_DENSE_PICK
+    const int threads = sv ? kDenseSvThreads : kDenseThreads;
+    const size_t smem = sv ? sv_bytes : 0;
+    if (sv) set_smem_once(kern, smem, (int)std::min<size_t>(100, (smem + 1024 + 2331) * 100 / (228 * 1024)));
     // resident CTAs per SM of the chosen instance (looked up once per instance and device)
     static std::mutex occ_mu;
     static std::map<std::pair<const void*, int>, int> occ_cache;
@@ -800,20 +912,20 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
       std::lock_guard<std::mutex> lk(occ_mu);
       int& o = occ_cache[{reinterpret_cast<const void*>(kern), dev}];
       if (!o) {
-        TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kDenseThreads, 0));
+        TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, sv ? (size_t)TK_DENSE_SV_MAX : 0));
         o = std::max(o, 1);
       }
       occ = o;
     }
-    const long long wpb = kDenseThreads / 32;
+    const long long wpb = threads / 32;
     const long long warps = std::min(nspans, (long long)num_sms() * occ * wpb);
     const long long blocks = (warps + wpb - 1) / wpb;
     ktimer_begin(st);
-    kern<<<(unsigned)blocks, kDenseThreads, 0, st>>>(p, nspans, ticket);
-    ktimer_end(st);
-    count_launch(2);
+    kern<<<(unsigned)blocks, threads, smem, st>>>(p, nspans);
     dense_fixup_kernel<<<(unsigned)((nspans + 255) / 256), 256, 0, st>>>(nspans, p.c_first, p.c_last, p.c_lastkey,
                                                                          p.c_flags, shape[0], out);
+    ktimer_end(st);
+    count_launch(2);
     TK_CUDA(cudaGetLastError());
     TK_CUDA(cudaMemcpyAsync(hc, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     TK_CUDA(cudaStreamSynchronize(st));
