@@ -116,6 +116,22 @@ int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const 
                             const int64_t* subs, const double* vals, int32_t keep, const double* const* vecs,
                             double* out, void* stream);
 
+/* Sparse MTTKRP: out(i_n, r) = sum over nonzeros of val * prod_{m != n} U_m(i_m, r), r < rank
+ * (rank <= 128).  factors: host array of d pointers (factors[n] ignored) to row-major
+ * (shape[m] x rank) matrices; out row-major (shape[n] x rank), dense.  Column r equals the
+ * multi-vector TTV of every mode but n with the vectors U_m(:, r) (the paper's named consumer
+ * of TTV; the reference has no MTTKRP, so its oracle is the reference's
+ * ttv_raw chained per column).  Each column is folded left to right in the kept mode's sorted
+ * row order (deterministic); canonical input with n == 0 streams without a sort, other modes
+ * sort row ids stably by subs[:, n] on the device.  Values within 1e-12 relative of the chain
+ * for non-cancelling data.  _device: cols/subs/vals/factors/out on the device; _host: all on
+ * the host (subs row-major (nnz, d)). */
+int tk_mttkrp_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                         const int64_t* subs, const double* vals, int32_t n, int64_t rank,
+                         const double* const* factors, double* out, void* stream);
+int tk_mttkrp_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
+                       int32_t n, int64_t rank, const double* const* factors, double* out);
+
 /* ---- synthetic operands (measurement inputs, generated on the device) ------------------- */
 
 /* Exactly nnz distinct coordinates of a d-way tensor, drawn per mode from a truncated

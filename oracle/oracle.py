@@ -151,6 +151,36 @@ def ttv_multi_dense(subs, vals, shape, vecs: dict, keep: int) -> np.ndarray:
     return out
 
 
+def mttkrp(subs, vals, shape, factors, n: int) -> np.ndarray:
+    """MTTKRP oracle: column r is ttv_multi_dense with the vectors factors[m][:, r].
+
+    The reference has no MTTKRP (the paper names it as future work, PAPER.md:18, 156, 273);
+    its definition here is the reference's own single-mode TTV chained per column
+    (ttv_raw, which is pinned to the reference's goldens), SURVEY.md §8 f4.
+    """
+    d = len(shape)
+    rank = next(np.asarray(f).shape[1] for m, f in enumerate(factors) if m != n)
+    out = np.zeros((shape[n], rank), dtype=np.float64)
+    for r in range(rank):
+        vecs = {m: np.ascontiguousarray(np.asarray(factors[m], dtype=np.float64)[:, r])
+                for m in range(d) if m != n}
+        out[:, r] = ttv_multi_dense(subs, vals, shape, vecs, n)
+    return out
+
+
+def mttkrp_fused(subs, vals, shape, factors, n: int) -> np.ndarray:
+    """Fused numpy restatement (row products, then a scatter-add) for larger cross-checks."""
+    subs = np.asarray(subs)
+    d = len(shape)
+    w = np.asarray(vals, dtype=np.float64)[:, None]
+    for m in range(d - 1, -1, -1):
+        if m != n:
+            w = w * np.asarray(factors[m], dtype=np.float64)[subs[:, m]]
+    out = np.zeros((shape[n], w.shape[1]), dtype=np.float64)
+    np.add.at(out, subs[:, n], w)
+    return out
+
+
 # -- the reference's own compiled module (oracle/_ref) ------------------------------------------
 
 def reference_module():

@@ -24,6 +24,7 @@ from .sparse import (
     SparseCooTensor,
     TtvRawResult,
     densify,
+    mttkrp,
     set_difference,
     ttv,
     unique_rows_accumulate,
@@ -56,6 +57,7 @@ __all__ = [
     "set_difference",
     "unique_rows_accumulate",
     "densify",
+    "mttkrp",
     "GENERATOR",
     "GenSpec",
     "gen_vector",

@@ -39,6 +39,10 @@ SIGNATURES = {
     "tk_group_sum_f64_host": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp, _vp, _c_i64p]),
     "tk_ttv_dense_f64_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp, _vp,
                                                ctypes.c_int32, _vp, _vp, _vp]),
+    "tk_mttkrp_f64_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp, _vp,
+                                            ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp]),
+    "tk_mttkrp_f64_host": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp,
+                                          ctypes.c_int32, ctypes.c_int64, _vp, _vp]),
     "tk_gen_coo_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, ctypes.c_double,
                                          ctypes.c_int32, ctypes.c_uint64, _vp, _vp, _vp]),
     "tk_gen_uniform_device": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, _vp, _vp]),

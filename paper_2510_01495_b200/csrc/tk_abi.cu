@@ -490,6 +490,79 @@ int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const 
   return ttv_dense_device(d, shape, nnz, cp.data(), vals, keep, vecs, out, st);
 }
 
+// ---- MTTKRP (the R-column TTV) ------------------------------------------------
+
+static int mttkrp_check(int32_t d, const int64_t* shape, int64_t nnz, int32_t n, int64_t rank, const void* factors,
+                        const void* out) {
+  if (d < 2) return fail(TK_EORDER, fmt("mttkrp: tensor order must be at least 2, got %lld", d));
+  if (n < 0 || n >= d) return fail(TK_EMODE, fmt("mttkrp: mode %lld out of range for order-%lld tensor", n, d));
+  if (d > TK_MAX_ORDER) return fail(TK_EARG, "mttkrp: tensor order exceeds TK_MAX_ORDER");
+  if (rank < 0 || rank > 128) return fail(TK_EARG, "mttkrp: rank must be in [0, 128]");
+  if (nnz < 0 || !shape || !factors || !out) return fail(TK_EARG, "mttkrp: bad arguments");
+  for (int m = 0; m < d; ++m)
+    if (shape[m] <= 0) return fail(TK_EARG, "mttkrp: shape entries must be positive");
+  return TK_OK;
+}
+
+int tk_mttkrp_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                         const int64_t* subs, const double* vals, int32_t n, int64_t rank,
+                         const double* const* factors, double* out, void* stream) {
+  CallClock clock_;
+  if (int rc = mttkrp_check(d, shape, nnz, n, rank, factors, out)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DevBuf soa;
+  std::vector<const int64_t*> cp(d);
+  if (cols) {
+    for (int m = 0; m < d; ++m) cp[m] = cols[m];
+  } else {
+    const int64_t pitch = pitch_of(nnz);
+    if (int rc = soa.alloc((size_t)pitch * d * 8, st)) return rc;
+    if (int rc = aos_to_soa(nnz, d, subs, soa.as<int64_t>(), pitch, st)) return rc;
+    for (int m = 0; m < d; ++m) cp[m] = soa.as<int64_t>() + (size_t)m * pitch;
+  }
+  return mttkrp_device(d, shape, nnz, cp.data(), vals, n, rank, factors, out, st);
+}
+
+int tk_mttkrp_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
+                       int32_t n, int64_t rank, const double* const* factors, double* out) {
+  CallClock clock_;
+  if (int rc = mttkrp_check(d, shape, nnz, n, rank, factors, out)) return rc;
+  cudaStream_t st = lib_stream();
+  const int64_t pitch = pitch_of(nnz);
+  size_t fac_elems = 0;
+  for (int m = 0; m < d; ++m)
+    if (m != n) fac_elems += (size_t)pitch_of(shape[m] * rank);
+  DevBuf b_aos, b_soa, b_vals, b_fac, b_out;
+  if (int rc = b_aos.alloc((size_t)std::max<int64_t>(nnz, 1) * d * 8, st)) return rc;
+  if (int rc = b_soa.alloc((size_t)pitch * d * 8 + 8, st)) return rc;
+  if (int rc = b_vals.alloc((size_t)pitch * 8 + 8, st)) return rc;
+  if (int rc = b_fac.alloc(fac_elems * 8 + 8, st)) return rc;
+  if (int rc = b_out.alloc((size_t)shape[n] * rank * 8 + 8, st)) return rc;
+  if (nnz) {
+    TK_CUDA(cudaMemcpyAsync(b_aos.get(), subs, (size_t)nnz * d * 8, cudaMemcpyHostToDevice, st));
+    TK_CUDA(cudaMemcpyAsync(b_vals.get(), vals, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+    if (int rc = aos_to_soa(nnz, d, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
+  }
+  std::vector<const double*> fp(d, nullptr);
+  std::vector<const int64_t*> cp(d);
+  size_t off = 0;
+  for (int m = 0; m < d; ++m) {
+    cp[m] = b_soa.as<int64_t>() + (size_t)m * pitch;
+    if (m == n) continue;
+    double* dst = b_fac.as<double>() + off;
+    if (shape[m] * rank)
+      TK_CUDA(cudaMemcpyAsync(dst, factors[m], (size_t)shape[m] * rank * 8, cudaMemcpyHostToDevice, st));
+    fp[m] = dst;
+    off += (size_t)pitch_of(shape[m] * rank);
+  }
+  if (int rc = mttkrp_device(d, shape, nnz, cp.data(), b_vals.as<double>(), n, rank, fp.data(), b_out.as<double>(), st))
+    return rc;
+  if (shape[n] * rank)
+    TK_CUDA(cudaMemcpyAsync(out, b_out.get(), (size_t)shape[n] * rank * 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
 // ---- generators -------------------------------------------------------------------------------
 
 int tk_gen_coo_device(int32_t d, const int64_t* shape, int64_t nnz, double zipf_s, int32_t normal_vals,

@@ -79,6 +79,8 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
                      int keep, const double* const* vecs, double* out, cudaStream_t st);
 
 // row-major (nnz, d) -> SoA columns with the given pitch (elements)
+int mttkrp_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals, int mode,
+                  int64_t R, const double* const* factors, double* out, cudaStream_t st);
 int aos_to_soa(int64_t nnz, int d, const int64_t* aos, int64_t* soa, int64_t pitch, cudaStream_t st);
 
 int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStream_t st);

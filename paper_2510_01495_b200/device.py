@@ -105,6 +105,20 @@ class DeviceCoo:
         return out
 
 
+    def mttkrp(self, factors: dict, n: int, out=None, stream=None):
+        """Mode-``n`` MTTKRP with row-major device factors ``{m: (shape[m], R)}``; dense
+        float64[(shape[n], R)] (tk_mttkrp_f64_device)."""
+        d = self.ndim
+        rank = int(next(iter(factors.values())).shape[1])
+        if out is None:
+            out = torch.empty((self.shape[n], rank), dtype=torch.float64, device=self.device)
+        ptrs = [0 if m == n else factors[m].data_ptr() for m in range(d)]
+        _lib.check(_lib.load().tk_mttkrp_f64_device(
+            d, _lib.i64_array(self.shape), self.nnz, _lib.ptr_array([c.data_ptr() for c in self.cols]), None,
+            self.vals.data_ptr(), int(n), rank, _lib.ptr_array(ptrs), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+
 def uniform_vector(n: int, seed: int, device="cuda", stream=None) -> torch.Tensor:
     out = torch.empty(n, dtype=torch.float64, device=device)
     _lib.check(_lib.load().tk_gen_uniform_device(n, int(seed) & (2**64 - 1), out.data_ptr(), _stream_handle(stream)))

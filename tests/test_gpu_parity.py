@@ -423,3 +423,62 @@ def test_dense_kernel_errors_and_unsorted(oracle):
     out = t.ttv_dense(vecs, 0).cpu().numpy()
     ref = oracle.ttv_multi_dense(subs[perm], vals[perm], shape, hv, 0)
     assert out.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("shape,nnz,R,n", [
+    ((200, 30, 40, 50), 60000, 16, 0),    # canonical n == 0: streams without a sort
+    ((200, 30, 40, 50), 60000, 16, 2),    # other mode: device sort of the row ids
+    ((5000, 3, 3, 3), 20000, 7, 0),       # runs of ~4 rows, rank not a multiple of 32
+    ((1, 700, 800), 150000, 32, 0),       # one run over ~150 spans (carries + fix-up)
+    ((60, 50), 2000, 40, 1),              # order 2, rank > 32 (two columns per lane)
+    ((12, 5, 6, 7, 8, 3), 20000, 3, 0),   # order 6: the any-order instance
+    ((40, 40, 40), 3001, 128, 1),         # rank 128 (four columns per lane)
+])
+def test_mttkrp_matches_chained_ttv_oracle(oracle, shape, nnz, R, n):
+    """MTTKRP through the host C ABI and the device entry point: within
+    1e-12 of the chained-TTV oracle, deterministic, zero rows for absent keys."""
+    import torch
+    import paper_2510_01495_b200 as tk
+    from paper_2510_01495_b200.device import DeviceCoo
+    subs, vals = _canonical_coo(shape, nnz, seed=nnz + R)
+    rng = np.random.default_rng(R)
+    U = [rng.random((s, R)) + 0.5 for s in shape]
+    t = tk.SparseCooTensor(subs, vals, shape)
+    got = tk.mttkrp(t, U, n)
+    ref = oracle.mttkrp(subs, vals, shape, U, n) if R * nnz <= 2_000_000 else \
+        oracle.mttkrp_fused(subs, vals, shape, U, n)
+    nz = ref != 0
+    assert np.array_equal(got != 0, nz)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz], initial=0.0) <= REL
+    dt = DeviceCoo.from_host(subs, vals, shape)
+    fac = {m: torch.from_numpy(U[m]).cuda() for m in range(len(shape)) if m != n}
+    dev = dt.mttkrp(fac, n).cpu().numpy()
+    assert dev.tobytes() == got.tobytes()
+    assert dt.mttkrp(fac, n).cpu().numpy().tobytes() == dev.tobytes()
+
+
+def test_mttkrp_errors_and_unsorted_input(oracle):
+    import paper_2510_01495_b200 as tk
+    from paper_2510_01495_b200.device import DeviceCoo
+    from paper_2510_01495_b200.errors import DimensionError, ModeError
+    import torch
+    shape = (30, 20, 20)
+    subs, vals = _canonical_coo(shape, 3000, seed=4)
+    U = [np.random.default_rng(m).random((s, 4)) + 0.5 for m, s in enumerate(shape)]
+    t = tk.SparseCooTensor(subs, vals, shape)
+    with pytest.raises(ModeError):
+        tk.mttkrp(t, U, 3)
+    with pytest.raises(DimensionError):
+        tk.mttkrp(t, [U[0], U[1][:10], U[2]], 0)
+    bad = subs.copy()
+    bad[100, 2] = 20
+    fac = {m: torch.from_numpy(U[m]).cuda() for m in (1, 2)}
+    with pytest.raises(DimensionError):
+        DeviceCoo.from_host(bad, vals, shape).mttkrp(fac, 0)
+    # rows out of kept-key order: detected, sorted on the device, same values as canonical
+    perm = np.random.default_rng(2).permutation(len(vals))
+    got = DeviceCoo.from_host(subs[perm], vals[perm], shape).mttkrp(fac, 0).cpu().numpy()
+    ref = oracle.mttkrp(subs[perm], vals[perm], shape, U, 0)
+    nz = ref != 0
+    assert np.array_equal(got != 0, nz)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= REL
