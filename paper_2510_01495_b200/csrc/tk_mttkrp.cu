@@ -36,9 +36,10 @@ constexpr int kMtWarps = kMtThreads / 32;
 
 struct MtParams {
   long long n;                     // rows
-  int d, mode;                     // order, kept mode n
+  int d;                           // order
+  int mode;                        // kept mode n in the caller's numbering (column 0 here)
   long long R;                     // rank (columns)
-  const long long* col[kMaxOrder];
+  const long long* col[kMaxOrder];  // col[0]: the kept mode; col[1..d-1]: the others, ascending
   const double* vals;
   const long long* perm;           // row order (nullptr: identity, keys already sorted)
   const double* fac[kMaxOrder];    // U_m, row-major (dims[m] x R); fac[mode] unused
@@ -51,110 +52,167 @@ struct MtParams {
   Counters* ctr;
 };
 
-// D: tensor order (2..5, gathers unrolled) or 0 (any order); RPL: columns per lane.
-template <int D, int RPL, bool PERM>
+// D: tensor order (2..5, gathers unrolled) or 0 (any order).  RP: lanes per row (a power of two
+// >= R for R <= 32, so a warp step covers G = 32/RP rows); RPL: columns per lane (R > 32, RP = 32).
+// Slot s = lane / RP handles rows j0+s of each G-row group and keeps its own partial of the open
+// run; a group with a head reduces the slot partials (xor butterfly over the slot bits) and walks
+// the group's rows in order, so each column is folded in a fixed order (deterministic).
+template <int D, int RP, int RPL, bool PERM>
 __global__ void __launch_bounds__(kMtThreads) mttkrp_kernel(MtParams p, long long nspans) {
   constexpr int DM = D > 0 ? D : kMaxOrder;
-  __shared__ long long s_idx[kMtWarps][DM][32];
+  constexpr int G = 32 / RP;
+  constexpr int B = 8 / RPL;  // groups per gather batch
+  static_assert(RP == 32 || RPL == 1, "several columns per lane only with full-warp rows");
+  __shared__ long long s_off[kMtWarps][DM][32];  // factor-row offsets idx*R (column 0 unused)
+  __shared__ long long s_key[kMtWarps][32];
   __shared__ double s_val[kMtWarps][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int slot = lane / RP, cl = lane % RP;
   const int d = D > 0 ? D : p.d;
-  const int mode = p.mode;
   const long long R = p.R;
-  const unsigned long long nkeep = (unsigned long long)p.dims[mode];
+  const unsigned long long nkeep = (unsigned long long)p.dims[0];  // the kept mode is column 0
   const long long W = ((long long)gridDim.x * blockDim.x) >> 5;
   unsigned int flags = 0;
   auto row_of = [&](long long q) { return PERM ? p.perm[q] : q; };
+  auto reduce_slots = [&](double v) {
+#pragma unroll
+    for (int o = RP; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;  // identical in every slot (RN addition commutes)
+  };
 
   for (long long sp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sp < nspans; sp += W) {
     const long long s0 = sp * kMtSpan, s1 = min(s0 + kMtSpan, p.n);
-    long long curkey = s0 > 0 ? p.col[mode][row_of(s0 - 1)] : 0;
+    long long curkey = s0 > 0 ? p.col[0][row_of(s0 - 1)] : 0;
     double acc[RPL];
 #pragma unroll
     for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
     bool seen = false;
     // a run closes at a head: the span's first closing before any head is its leading carry
-    auto flush = [&](long long key) {
+    auto flush = [&](long long key, const double* tot) {
+      if (slot != 0) return;
       if (!seen) {
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
-          const long long c = lane + 32 * q;
-          if (c < R) p.c_first[sp * R + c] = acc[q];
+          const long long c = cl + 32 * q;
+          if (c < R) p.c_first[sp * R + c] = tot[q];
         }
       } else if ((unsigned long long)key < nkeep) {
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
-          const long long c = lane + 32 * q;
-          if (c < R) p.out[key * R + c] = acc[q];
+          const long long c = cl + 32 * q;
+          if (c < R) p.out[key * R + c] = tot[q];
         }
       }
     };
     for (long long b = s0; b < s1; b += 32) {
-      // stage 32 rows (coalesced loads; the permuted path reads through perm)
+      // stage 32 rows (coalesced loads; the permuted path reads through perm).  Per row, once:
+      // the factor-row offsets idx*R (bounds-checked: an out-of-range index raises and is never
+      // read), the head bit (key change) and the order / kept-bounds checks.
       const long long q0 = b + lane;
-      if (q0 < s1) {
+      const bool ok = q0 < s1;
+      long long key = curkey;
+      if (ok) {
         const long long row = row_of(q0);
-        for (int m = 0; m < d; ++m) s_idx[wib][m][lane] = p.col[m][row];
+        key = p.col[0][row];
+#pragma unroll
+        for (int m = 1; m < DM; ++m) {
+          if (D == 0 && m >= d) break;
+          const long long idx = p.col[m][row];
+          const bool bad = (unsigned long long)idx >= (unsigned long long)p.dims[m];
+          if (bad) flags |= kFlagIndex;
+          s_off[wib][m][lane] = (bad ? 0 : idx) * R;
+        }
         s_val[wib][lane] = p.vals[row];
       }
+      long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+      if (lane == 0) prev = curkey;
+      const bool head = ok && (q0 == 0 || key != prev);
+      if (head && q0 > 0 && key < prev) flags |= kFlagUnsorted;
+      if (head && (unsigned long long)key >= nkeep) flags |= kFlagKeptOob;
+      const unsigned int hmask = __ballot_sync(0xffffffffu, head);
+      s_key[wib][lane] = key;
       __syncwarp();
       const int cnt = (int)min(32LL, s1 - b);
-      for (int j = 0; j < cnt; ++j) {
-        const long long key = s_idx[wib][mode][j];
-        const bool head = (b + j == 0) || key != curkey;
-        if (head) {
-          if (b + j > 0 && key < curkey) flags |= kFlagUnsorted;
-          if ((unsigned long long)key >= nkeep) flags |= kFlagKeptOob;
-          flush(curkey);
-          seen = true;
-          curkey = key;
+      for (int j0 = 0; j0 < cnt; j0 += B * G) {
+        // every gather of the batch (B groups of G rows) in flight before the first product
+        double g[B][RPL][DM];
 #pragma unroll
-          for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
+        for (int bb = 0; bb < B; ++bb) {
+          const int j = min(j0 + bb * G + slot, cnt - 1);  // past the block: a repeated row, unused
+#pragma unroll
+          for (int m = 1; m < DM; ++m) {
+            if (D == 0 && m >= d) break;
+            const double* row = p.fac[m] + s_off[wib][m][j];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+              const long long c = cl + 32 * q;
+              g[bb][q][m] = c < R ? __ldg(row + c) : 0.0;
+            }
+          }
         }
-        // gathers first (all in flight), then the products in descending mode order
-        double g[RPL][DM];
 #pragma unroll
-        for (int m = 0; m < DM; ++m) {
-          if (D == 0 && m >= d) break;
-          if (m == mode) continue;
-          const long long idx = s_idx[wib][m][j];
-          const bool bad = (unsigned long long)idx >= (unsigned long long)p.dims[m];
-          if (bad) flags |= kFlagIndex;  // the call raises; never read out of range
-          const double* row = p.fac[m] + (bad ? 0 : idx) * R;
+        for (int bb = 0; bb < B; ++bb) {
+          const int jg = j0 + bb * G;  // first row of the group
+          if (jg >= cnt) break;
+          const int j = jg + slot;
+          const double v = j < cnt ? s_val[wib][j] : 0.0;
+          double w[RPL];
 #pragma unroll
           for (int q = 0; q < RPL; ++q) {
-            const long long c = lane + 32 * q;
-            g[q][m] = c < R ? __ldg(row + c) : 0.0;
-          }
-        }
-        const double v = s_val[wib][j];
+            w[q] = v;
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          double w = v;
-#pragma unroll
-          for (int m = DM - 1; m >= 0; --m) {
-            if (D == 0 && m >= d) continue;
-            if (m == mode) continue;
-            w = __dmul_rn(w, g[q][m]);
+            for (int m = DM - 1; m >= 1; --m) {  // descending modes: the chained-TTV association
+              if (D == 0 && m >= d) continue;
+              w[q] = __dmul_rn(w[q], g[bb][q][m]);
+            }
           }
-          acc[q] = __dadd_rn(acc[q], w);
+          const unsigned int gm = (hmask >> jg) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
+          if (gm == 0) {
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) acc[q] = __dadd_rn(acc[q], w[q]);
+            continue;
+          }
+          // the group holds a head: slot partials -> one total, then the rows in order
+          double tot[RPL];
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) tot[q] = reduce_slots(acc[q]);
+#pragma unroll
+          for (int s = 0; s < G; ++s) {
+            if (jg + s >= cnt) break;
+            double ws[RPL];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) ws[q] = __shfl_sync(0xffffffffu, w[q], s * RP + cl);
+            if ((gm >> s) & 1u) {
+              flush(curkey, tot);
+              seen = true;
+              curkey = s_key[wib][jg + s];
+#pragma unroll
+              for (int q = 0; q < RPL; ++q) tot[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) tot[q] = __dadd_rn(tot[q], ws[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) acc[q] = slot == 0 ? tot[q] : 0.0;
         }
       }
+      curkey = s_key[wib][cnt - 1];
       __syncwarp();
     }
     // span end: the trailing run is closed here unless the next row continues it
-    const bool last_open = s1 < p.n && p.col[mode][row_of(s1)] == curkey;
-    if (!seen) {
-      flush(curkey);  // the whole span continues the run open at its start: leading carry
-    } else if (last_open) {
+    double tot[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) tot[q] = reduce_slots(acc[q]);
+    const bool last_open = s1 < p.n && p.col[0][row_of(s1)] == curkey;
+    if (!seen || !last_open) {
+      flush(curkey, tot);  // !seen: the whole span continues the run open at its start
+    } else if (slot == 0) {
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
-        const long long c = lane + 32 * q;
-        if (c < R) p.c_last[sp * R + c] = acc[q];
+        const long long c = cl + 32 * q;
+        if (c < R) p.c_last[sp * R + c] = tot[q];
       }
       if (lane == 0) p.c_lastkey[sp] = curkey;
-    } else {
-      flush(curkey);
     }
     if (lane == 0) p.c_flags[sp] = (seen ? 1 : 0) | (last_open ? 2 : 0);
   }
@@ -186,21 +244,21 @@ __global__ void iota_kernel(long long n, long long* __restrict__ v) {
     v[i] = i;
 }
 
-template <int D, int RPL>
+template <int D, int RP, int RPL>
 void* pick_mt(bool perm) {
-  return perm ? reinterpret_cast<void*>(mttkrp_kernel<D, RPL, true>)
-              : reinterpret_cast<void*>(mttkrp_kernel<D, RPL, false>);
+  return perm ? reinterpret_cast<void*>(mttkrp_kernel<D, RP, RPL, true>)
+              : reinterpret_cast<void*>(mttkrp_kernel<D, RP, RPL, false>);
 }
 
-template <int RPL>
-void* pick_mt_d(int d, bool perm) {
-  switch (d) {
-    case 2: return pick_mt<2, RPL>(perm);
-    case 3: return pick_mt<3, RPL>(perm);
-    case 4: return pick_mt<4, RPL>(perm);
-    case 5: return pick_mt<5, RPL>(perm);
-    default: return pick_mt<0, RPL>(perm);
-  }
+// rank -> (lanes per row, columns per lane) instance for an order-D tensor
+template <int D>
+void* pick_mt_r(long long R, bool perm) {
+  if (R > 64) return pick_mt<D, 32, 4>(perm);
+  if (R > 32) return pick_mt<D, 32, 2>(perm);
+  if (D == 0 || R > 16) return pick_mt<D, 32, 1>(perm);
+  if (R > 8) return pick_mt<D == 0 ? 2 : D, 16, 1>(perm);
+  if (R > 4) return pick_mt<D == 0 ? 2 : D, 8, 1>(perm);
+  return pick_mt<D == 0 ? 2 : D, 4, 1>(perm);
 }
 
 int launch_mttkrp(MtParams& p, bool perm, cudaStream_t st, unsigned int* flags_out) {
@@ -216,8 +274,9 @@ int launch_mttkrp(MtParams& p, bool perm, cudaStream_t st, unsigned int* flags_o
   p.c_flags = reinterpret_cast<int*>(b + 2 * per + perk);
   p.ctr = reinterpret_cast<Counters*>(b + 2 * per + 2 * perk);
   TK_CUDA(cudaMemsetAsync(p.ctr, 0, sizeof(Counters), st));
-  const int rpl = (int)((p.R + 31) / 32);
-  void* kern = rpl <= 1 ? pick_mt_d<1>(p.d, perm) : rpl <= 2 ? pick_mt_d<2>(p.d, perm) : pick_mt_d<4>(p.d, perm);
+  void* kern = p.d == 2 ? pick_mt_r<2>(p.R, perm) : p.d == 3 ? pick_mt_r<3>(p.R, perm)
+               : p.d == 4 ? pick_mt_r<4>(p.R, perm) : p.d == 5 ? pick_mt_r<5>(p.R, perm)
+                                                     : pick_mt_r<0>(p.R, perm);
   const long long warps = std::min(nspans, (long long)num_sms() * 8 * kMtWarps);
   const unsigned blocks = (unsigned)((warps + kMtWarps - 1) / kMtWarps);
   void* args[] = {&p, const_cast<long long*>(&nspans)};
@@ -225,7 +284,7 @@ int launch_mttkrp(MtParams& p, bool perm, cudaStream_t st, unsigned int* flags_o
   TK_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kMtThreads), args, 0, st));
   const long long nfix = nspans * p.R;
   mttkrp_fixup_kernel<<<(unsigned)((nfix + 255) / 256), 256, 0, st>>>(nspans, p.R, p.c_first, p.c_last,
-                                                                       p.c_lastkey, p.c_flags, p.dims[p.mode], p.out);
+                                                                       p.c_lastkey, p.c_flags, p.dims[0], p.out);
   ktimer_end(st);
   count_launch(2);
   TK_CUDA(cudaGetLastError());
@@ -247,10 +306,13 @@ int mttkrp_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const
   p.d = d;
   p.mode = mode;
   p.R = R;
-  for (int m = 0; m < d; ++m) {
-    p.col[m] = reinterpret_cast<const long long*>(cols[m]);
-    p.fac[m] = factors[m];
-    p.dims[m] = shape[m];
+  // kept mode first, then the others in ascending order: the kernel's descending walk over
+  // columns 1..d-1 is then the chained-TTV association (descending modes, skipping n)
+  for (int m = 0, c = 1; m < d; ++m) {
+    const int q = m == mode ? 0 : c++;
+    p.col[q] = reinterpret_cast<const long long*>(cols[m]);
+    p.fac[q] = factors[m];
+    p.dims[q] = shape[m];
   }
   p.vals = vals;
   p.out = out;

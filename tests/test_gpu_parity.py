@@ -433,6 +433,9 @@ def test_dense_kernel_errors_and_unsorted(oracle):
     ((60, 50), 2000, 40, 1),              # order 2, rank > 32 (two columns per lane)
     ((12, 5, 6, 7, 8, 3), 20000, 3, 0),   # order 6: the any-order instance
     ((40, 40, 40), 3001, 128, 1),         # rank 128 (four columns per lane)
+    ((300, 40, 50), 200000, 3, 0),        # rank 3: eight rows per warp step, runs cross groups
+    ((3000, 9, 9), 30000, 1, 0),          # rank 1 (the multi-vector TTV), short runs
+    ((50, 20, 20, 20), 4099, 12, 3),      # last mode kept (sorted path), odd row count
 ])
 def test_mttkrp_matches_chained_ttv_oracle(oracle, shape, nnz, R, n):
     """MTTKRP through the host C ABI and the device entry point: within
