@@ -268,6 +268,17 @@ def secondary_measurements(rank, steps):
     ms = kernel_ms(lambda: t4.ttv_dense(vecs, 0, out4))
     b = c4["nnz"] * 40 + 3 * 8 * 20000 + 8 * 20000
     res["cfg4_ttv_dense"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c4["nnz"] / ms * 1e3, "bytes": b}
+    # extension (not a BASELINE config): MTTKRP of the config-4 tensor, mode 0,
+    # rank 16; bytes = the stream + factor matrices + output (the R-wide gathers hit L2)
+    R = 16
+    gen = torch.Generator(device="cuda").manual_seed(16)
+    fac = {m: torch.rand((c4["shape"][m], R), dtype=torch.float64, device="cuda", generator=gen) for m in (1, 2, 3)}
+    out_m = torch.empty((c4["shape"][0], R), dtype=torch.float64, device="cuda")
+    ms = kernel_ms(lambda: t4.mttkrp(fac, 0, out_m))
+    b = c4["nnz"] * 40 + 4 * 8 * 20000 * R
+    res["ext_mttkrp_cfg4_r16"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c4["nnz"] / ms * 1e3,
+                                  "bytes": b, "gathered_GBps": c4["nnz"] * 3 * R * 8 / ms / 1e6}
+    del fac, out_m
     del t4
     torch.cuda.empty_cache()
     return res
