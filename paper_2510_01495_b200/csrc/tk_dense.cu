@@ -17,7 +17,7 @@ namespace tk {
 
 namespace {
 constexpr int kDotThreads = 256;
-constexpr int kDotUnroll = 4;
+constexpr int kDotUnroll = 2;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -39,10 +39,18 @@ __device__ __forceinline__ double block_sum(double v, double* s_warp) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double* __restrict__ x,
-                                                                  const double* __restrict__ y, long long n,
-                                                                  double* __restrict__ partial, int vec2) {
+// Single pass: every CTA streams its grid-stride share with all kDotUnroll 16-byte load pairs in
+// flight, reduces it (warp butterflies, fixed warp order), stores its partial and takes a ticket;
+// the last CTA to finish sums the partials in CTA-index order (thread t takes t, t+256, ...; then
+// the same block tree), so the result does not depend on which CTA finished when.  The ticket
+// word is zeroed by the host (cudaMemsetAsync) before the launch.
+__global__ void __launch_bounds__(kDotThreads) dot_kernel(const double* __restrict__ x,
+                                                          const double* __restrict__ y, long long n,
+                                                          double* __restrict__ partial,
+                                                          unsigned int* __restrict__ ticket,
+                                                          double* __restrict__ out, int vec2) {
   __shared__ double s_warp[kDotThreads / 32];
+  __shared__ bool s_last;
   double acc = 0.0;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -64,26 +72,40 @@ __global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double* 
         acc = __dadd_rn(acc, __dmul_rn(a[u].y, b[u].y));
       }
     }
-    for (; i < n2; i += stride) {
-      const double2 a = __ldcs(x2 + i), b = __ldcs(y2 + i);
-      acc = __dadd_rn(acc, __dmul_rn(a.x, b.x));
-      acc = __dadd_rn(acc, __dmul_rn(a.y, b.y));
+    {  // remainder: fewer than kDotUnroll strides left, still all loads first
+      double2 a[kDotUnroll - 1], b[kDotUnroll - 1];
+#pragma unroll
+      for (int u = 0; u < kDotUnroll - 1; ++u) {
+        const bool ok = i + u * stride < n2;
+        a[u] = ok ? __ldcs(x2 + i + u * stride) : make_double2(0.0, 0.0);
+        b[u] = ok ? __ldcs(y2 + i + u * stride) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kDotUnroll - 1; ++u) {
+        if (i + u * stride < n2) {
+          acc = __dadd_rn(acc, __dmul_rn(a[u].x, b[u].x));
+          acc = __dadd_rn(acc, __dmul_rn(a[u].y, b[u].y));
+        }
+      }
     }
     if ((n & 1) && tid == 0) acc = __dadd_rn(acc, __dmul_rn(x[n - 1], y[n - 1]));
   } else {
     for (long long i = tid; i < n; i += stride) acc = __dadd_rn(acc, __dmul_rn(x[i], y[i]));
   }
   const double s = block_sum(acc, s_warp);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(kDotThreads) dot_final_kernel(const double* __restrict__ partial, int nblk,
-                                                                double* __restrict__ out) {
-  __shared__ double s_warp[kDotThreads / 32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc = __dadd_rn(acc, partial[i]);
-  const double s = block_sum(acc, s_warp);
-  if (threadIdx.x == 0) *out = s;
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = s;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) t = __dadd_rn(t, __ldcg(partial + b));
+  __syncthreads();  // s_warp reuse
+  const double r = block_sum(t, s_warp);
+  if (threadIdx.x == 0) *out = r;
 }
 
 // One warp per row; 128-bit loads of the row (streamed), x through the read-only path (L1
@@ -133,6 +155,8 @@ __global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __r
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int dot_blocks(long long n) {
+  // one grid-stride round of kDotUnroll 16-byte load pairs per thread when that fits eight
+  // 256-thread CTAs per SM (config 1: 977 CTAs, every load of the call in flight at once)
   const long long want = (n + 2LL * kDotThreads * kDotUnroll - 1) / (2LL * kDotThreads * kDotUnroll);
   return (int)std::max(1LL, std::min(want, (long long)num_sms() * 8));
 }
@@ -143,14 +167,14 @@ int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStr
     return TK_OK;
   }
   const int nblk = dot_blocks(n);
-  DevBuf part;
-  if (int rc = part.alloc((size_t)nblk * sizeof(double), st)) return rc;
+  DevBuf part;  // [ticket (8 B) | partials]
+  if (int rc = part.alloc((size_t)(nblk + 1) * sizeof(double), st)) return rc;
+  TK_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double), st));
   const int vec2 = al16(x) && al16(y);
   ktimer_begin(st);
-  dot_partial_kernel<<<nblk, kDotThreads, 0, st>>>(x, y, n, part.as<double>(), vec2);
-  dot_final_kernel<<<1, kDotThreads, 0, st>>>(part.as<double>(), nblk, out);
+  dot_kernel<<<nblk, kDotThreads, 0, st>>>(x, y, n, part.as<double>() + 1, part.as<unsigned int>(), out, vec2);
   ktimer_end(st);
-  count_launch(2);
+  count_launch();
   TK_CUDA(cudaGetLastError());
   return TK_OK;
 }

@@ -74,7 +74,7 @@ def test_config1_dot_full_size(K, oracle, golden_hashes):
     ref = float.fromhex(golden_hashes["cfg1"]["dot_hex"])
     got = K.dot(ops["x"], ops["y"])
     assert abs(got - ref) <= REL * abs(ref)
-    for n in (1, 2, 3, 17, 1023, 4097, 100001):
+    for n in (1, 2, 3, 17, 1023, 4097, 100001, 2_400_001, 10_000_000):
         x, y = np.random.default_rng(n).random(n), np.random.default_rng(n + 1).random(n)
         r = oracle.dot(x, y)
         assert abs(K.dot(x, y) - r) <= REL * abs(r)
