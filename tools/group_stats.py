@@ -10,10 +10,10 @@ key = t.cols[0] * shape[1] + t.cols[1]
 _, counts = torch.unique_consecutive(key, return_counts=True)
 c = counts.double()
 print(f"nnz={nnz} groups={counts.numel()} mean={c.mean():.2f} max={int(counts.max())}")
-for th in (1, 2, 8, 32, 64, 256, 1024, 4096):
+for th in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 768, 1024, 4096):
     m = counts > th
     print(f"  groups > {th:5d}: {int(m.sum()):10d}  rows in them: {float(c[m].sum())/nnz*100:6.2f}%")
-tile = 1024
+tile = int(sys.argv[2]) if len(sys.argv) > 2 else 768
 starts = torch.cumsum(counts, 0) - counts
 ends = starts + counts
 span = (starts // tile) != ((ends - 1) // tile)
