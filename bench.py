@@ -289,6 +289,56 @@ def secondary_measurements(rank, steps):
     return res
 
 
+def multi_dense_measurement(rank, world, steps, warmup):
+    """Config 4 sharded across the ranks: the kernel-store merge
+    (multi.PeerDenseMerge: every shard's dense-TTV kernel stores its owned keep-mode range into
+    all ranks' NVLink-mapped output vectors, then a one-element barrier) against the NCCL
+    all-reduce merge of zero-padded partials.  Device time per step (CUDA events, max over
+    ranks); the two merged vectors must be bit-identical.  Requires an initialised process group."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_01495_b200 import multi
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    c4 = CFG4
+    shape = c4["shape"]
+    full = DeviceCoo.generate(shape, c4["nnz"], seed=c4["seed"])
+    vecs = {m: uniform_vector(shape[m], 40 + m) for m in (1, 2, 3)}
+    bounds = multi.shard_bounds(full.cols[0], world)
+    klo, khi = multi.owned_key_range(full.cols[0], bounds, rank, shape[0])
+    t = full.slice(bounds[rank], bounds[rank + 1]) if world > 1 else full
+    del full
+    torch.cuda.empty_cache()
+    merge = multi.PeerDenseMerge(shape[0], torch.cuda.current_device())
+    red = torch.empty(shape[0], dtype=torch.float64, device="cuda")
+
+    def peer_step():
+        merge.run(t, vecs, 0, klo, khi)
+
+    def nccl_step():
+        t.ttv_dense(vecs, 0, red)
+        dist.all_reduce(red)
+
+    res = {}
+    for name, fn in (("kernel_store_merge", peer_step), ("nccl_allreduce_merge", nccl_step)):
+        for _ in range(warmup):
+            fn()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+        res[name] = {"ms_per_step": ms, "nnz_per_s": c4["nnz"] / (ms / 1e3)}
+    res["identical"] = bool(torch.equal(merge.out, red))
+    res["workload"] = "cfg4_ttv_dense_20000^4_nnz1e8_keep0"
+    res["shard_rows"] = t.nnz
+    merge.close()
+    return res
+
+
 def run_ours(args):
     import torch
     from paper_2510_01495_b200 import _lib, multi
@@ -375,6 +425,12 @@ def run_ours(args):
         torch.cuda.empty_cache()
         secondary = secondary_measurements(rank, max(3, min(args.steps, 10)))
 
+    multi_dense = None
+    if world > 1 and not args.no_secondary:
+        del out_subs, out_vals
+        torch.cuda.empty_cache()
+        multi_dense = multi_dense_measurement(rank, world, max(3, min(args.steps, 10)), 3)
+
     if rank == 0 and world == 1 and not args.no_cpu:
         el, kind, _ = cpu_reference_ttv(subs_s, vals_s, shape, x.cpu().numpy(), k)
         cpu_leg = {"value": subs_s.shape[0] / el, "unit": "nnz/s", "cores": 1, "kind": kind,
@@ -401,6 +457,8 @@ def run_ours(args):
             "cpu_baseline": cpu_leg,
             "secondary": secondary,
         }
+        if multi_dense is not None:
+            line["multi_dense"] = multi_dense
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

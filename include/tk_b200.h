@@ -116,6 +116,28 @@ int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const 
                             const int64_t* subs, const double* vals, int32_t keep, const double* const* vecs,
                             double* out, void* stream);
 
+/* Sharded form of tk_ttv_dense_f64_device (SURVEY.md 8e, config 4 on N GPUs): this GPU's
+ * shard (rows split at keep-mode key changes) produces the result for keep-mode indices
+ * [key_lo, key_hi) -- zeros for indices without rows -- and stores it straight into every
+ * one of outs[0..nout) (host array of device pointers: this GPU's output vector and the
+ * peers' output vectors mapped over NVLink with tk_ipc_open).  The N shards together write
+ * every element of every copy exactly once, so after a barrier every GPU holds the full,
+ * bit-identical result: this replaces the all-reduce of the reference-style merge
+ * (multi.merge_dense) with the kernel's own epilogue stores.  nout <= 8. */
+int tk_ttv_dense_f64_device_peers(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                                  const double* vals, int32_t keep, const double* const* vecs,
+                                  double* const* outs, int32_t nout, int64_t key_lo, int64_t key_hi,
+                                  void* stream);
+
+/* CUDA IPC for the peer outputs: allocate / free an exportable device buffer (its own
+ * cudaMalloc, so the handle maps to its first byte), export it (64-byte handle), map a peer's
+ * exported buffer into this process (peer access enabled lazily), unmap it. */
+int tk_ipc_alloc(int64_t bytes, void** dev_ptr);
+int tk_ipc_free(void* dev_ptr);
+int tk_ipc_get_handle(const void* dev_ptr, void* handle64);
+int tk_ipc_open(const void* handle64, void** dev_ptr);
+int tk_ipc_close(void* dev_ptr);
+
 /* Sparse MTTKRP: out(i_n, r) = sum over nonzeros of val * prod_{m != n} U_m(i_m, r), r < rank
  * (rank <= 128).  factors: host array of d pointers (factors[n] ignored) to row-major
  * (shape[m] x rank) matrices; out row-major (shape[n] x rank), dense.  Column r equals the

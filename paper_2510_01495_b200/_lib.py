@@ -39,6 +39,14 @@ SIGNATURES = {
     "tk_group_sum_f64_host": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp, _vp, _c_i64p]),
     "tk_ttv_dense_f64_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp, _vp,
                                                ctypes.c_int32, _vp, _vp, _vp]),
+    "tk_ttv_dense_f64_device_peers": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp,
+                                                     ctypes.c_int32, _vp, _vp, ctypes.c_int32, ctypes.c_int64,
+                                                     ctypes.c_int64, _vp]),
+    "tk_ipc_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "tk_ipc_free": (ctypes.c_int, [_vp]),
+    "tk_ipc_get_handle": (ctypes.c_int, [_vp, _vp]),
+    "tk_ipc_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "tk_ipc_close": (ctypes.c_int, [_vp]),
     "tk_mttkrp_f64_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp, _vp,
                                             ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp]),
     "tk_mttkrp_f64_host": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp,

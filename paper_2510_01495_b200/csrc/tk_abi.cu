@@ -490,6 +490,58 @@ int tk_ttv_dense_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const 
   return ttv_dense_device(d, shape, nnz, cp.data(), vals, keep, vecs, out, st);
 }
 
+int tk_ttv_dense_f64_device_peers(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                                  const double* vals, int32_t keep, const double* const* vecs,
+                                  double* const* outs, int32_t nout, int64_t key_lo, int64_t key_hi,
+                                  void* stream) {
+  if (d < 2) return fail(TK_EORDER, fmt("ttv: tensor order must be at least 2, got %lld", d));
+  if (keep < 0 || keep >= d) return fail(TK_EMODE, fmt("ttv: mode %lld out of range for order-%lld tensor", keep, d));
+  if (d > TK_MAX_ORDER) return fail(TK_EARG, "ttv: tensor order exceeds TK_MAX_ORDER");
+  if (nnz < 0 || !shape || !vecs || !outs || !cols || nout < 1 || nout > 8)
+    return fail(TK_EARG, "ttv_dense_peers: bad arguments");
+  if (key_lo < 0 || key_hi > shape[keep] || key_lo > key_hi)
+    return fail(TK_EARG, "ttv_dense_peers: owned range outside the keep-mode dimension");
+  for (int i = 0; i < nout; ++i)
+    if (!outs[i]) return fail(TK_EARG, "ttv_dense_peers: null output");
+  return ttv_dense_peers(d, shape, nnz, cols, vals, keep, vecs, outs, nout, key_lo, key_hi,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int tk_ipc_alloc(int64_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes <= 0) return fail(TK_EARG, "ipc: bad allocation request");
+  TK_CUDA(cudaMalloc(dev_ptr, (size_t)bytes));
+  return TK_OK;
+}
+
+int tk_ipc_free(void* dev_ptr) {
+  if (!dev_ptr) return fail(TK_EARG, "ipc: null argument");
+  TK_CUDA(cudaFree(dev_ptr));
+  return TK_OK;
+}
+
+int tk_ipc_get_handle(const void* dev_ptr, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (!dev_ptr || !handle64) return fail(TK_EARG, "ipc: null argument");
+  cudaIpcMemHandle_t h;
+  TK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  memcpy(handle64, &h, sizeof h);
+  return TK_OK;
+}
+
+int tk_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!dev_ptr || !handle64) return fail(TK_EARG, "ipc: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  TK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TK_OK;
+}
+
+int tk_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(TK_EARG, "ipc: null argument");
+  TK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return TK_OK;
+}
+
 // ---- MTTKRP (the R-column TTV) ------------------------------------------------
 
 static int mttkrp_check(int32_t d, const int64_t* shape, int64_t nnz, int32_t n, int64_t rank, const void* factors,

@@ -14,6 +14,7 @@ namespace tk {
 
 constexpr int kMaxOrder = 16;              // largest tensor order the GPU path accepts
 constexpr int kMaxKeep = kMaxOrder - 1;    // kept (output) modes
+constexpr int kMaxPeers = 8;               // output copies of a sharded dense result (GPUs per node)
 
 // device-side status bits, collected in Counters::flags
 enum : unsigned int {

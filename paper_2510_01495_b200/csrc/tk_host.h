@@ -78,6 +78,14 @@ int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* c
 int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
                      int keep, const double* const* vecs, double* out, cudaStream_t st);
 
+// The same with the result for keep-mode indices [key_lo, key_hi) stored into every one of
+// outs[0..nout) (this GPU's vector and NVLink-mapped peer vectors: the sharded merge).
+int ttv_dense_peers(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    int keep, const double* const* vecs, double* const* outs, int nout, long long key_lo,
+                    long long key_hi, cudaStream_t st);
+int ttv_dense_chain(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    int keep, const double* const* vecs, double* out, cudaStream_t st);
+
 // row-major (nnz, d) -> SoA columns with the given pitch (elements)
 int mttkrp_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals, int mode,
                   int64_t R, const double* const* factors, double* out, cudaStream_t st);

@@ -164,7 +164,10 @@ struct DenseParams {
   const double* vals;
   const double* vec[kMaxOrder];
   long long dims[kMaxOrder];
-  double* out;
+  double* out;                 // == outs[0]
+  double* outs[kMaxPeers];     // every output copy: this GPU's vector and peers' (NVLink-mapped)
+  int nout;
+  long long key_lo, key_hi;    // keep-mode indices this call owns (stores outside are dropped)
   double* c_first;
   double* c_last;
   long long* c_lastkey;
@@ -186,6 +189,31 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;  // identical in every lane (RN addition commutes)
+}
+
+// One finished output element, stored into every output copy (this GPU and its peers: the
+// merge of the sharded dense result is these direct NVLink stores, no all-reduce).  Only the
+// keep-mode indices this call owns are stored; a shard split at key changes owns its keys.
+__device__ __forceinline__ void dense_store(const DenseParams& p, long long key, double v) {
+  if (key < p.key_lo || key >= p.key_hi) return;
+  for (int i = 0; i < p.nout; ++i) p.outs[i][key] = v;
+}
+
+// Zero the owned range [lo, hi) of every output copy (keys without rows stay 0).
+struct PeerOuts {
+  double* p[kMaxPeers];
+  int n;
+};
+__global__ void zero_range_kernel(PeerOuts o, long long lo, long long hi) {
+  for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi; i += (long long)gridDim.x * blockDim.x)
+    for (int c = 0; c < o.n; ++c) o.p[c][i] = 0.0;
+}
+// Copy [lo, hi) of src into every output copy (the chained fallback computes into src).
+__global__ void bcast_range_kernel(const double* __restrict__ src, PeerOuts o, long long lo, long long hi) {
+  for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi; i += (long long)gridDim.x * blockDim.x) {
+    const double v = src[i];
+    for (int c = 0; c < o.n; ++c) o.p[c][i] = v;
+  }
 }
 
 #ifndef TK_DENSE_SPAN
@@ -435,7 +463,7 @@ __global__ void __launch_bounds__(SV ? kDenseSvThreads : kDenseThreads, SV ? 1 :
         // span is the span's leading carry
         auto close = [&](bool cont, long long key, double v) {
           if (cont && !seen) p.c_first[fsp] = v;
-          else if ((unsigned long long)key < nkeep) p.out[key] = v;
+          else dense_store(p, key, v);
         };
         if (ha) close(!exc.f, pv, exc.f ? exc.v : __dadd_rn(tot, exc.v));
         if (hb) {
@@ -467,8 +495,8 @@ __global__ void __launch_bounds__(SV ? kDenseSvThreads : kDenseThreads, SV ? 1 :
         } else if (last_open) {
           p.c_last[fsp] = total;
           p.c_lastkey[fsp] = curkey;
-        } else if ((unsigned long long)curkey < nkeep) {
-          p.out[curkey] = total;
+        } else {
+          dense_store(p, curkey, total);
         }
         p.c_flags[fsp] = (seen ? 1 : 0) | (last_open ? 2 : 0);
       }
@@ -491,7 +519,7 @@ __global__ void __launch_bounds__(SV ? kDenseSvThreads : kDenseThreads, SV ? 1 :
 
 __global__ void dense_fixup_kernel(long long ntiles, const double* __restrict__ c_first,
                                    const double* __restrict__ c_last, const long long* __restrict__ c_lastkey,
-                                   const int* __restrict__ c_flags, long long nkeep, double* __restrict__ out) {
+                                   const int* __restrict__ c_flags, DenseParams p) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= ntiles || (c_flags[t] & 3) != 3) return;
   double s = c_last[t];
@@ -500,8 +528,7 @@ __global__ void dense_fixup_kernel(long long ntiles, const double* __restrict__ 
     const int f2 = c_flags[t2];
     if ((f2 & 1) || !(f2 & 2)) break;
   }
-  const long long k = c_lastkey[t];
-  if (k >= 0 && k < nkeep) out[k] = s;
+  dense_store(p, c_lastkey[t], s);
 }
 
 // ============================================================================================
@@ -855,8 +882,30 @@ int scatter_dense(long long n, const int64_t* idx, const double* v, double* out,
 
 int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
                      int keep, const double* const* vecs, double* out, cudaStream_t st) {
+  return ttv_dense_peers(d, shape, nnz, cols, vals, keep, vecs, &out, 1, 0, shape[keep], st);
+}
+
+int ttv_dense_peers(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    int keep, const double* const* vecs, double* const* outs, int nout, long long key_lo,
+                    long long key_hi, cudaStream_t st) {
   const long long nkeep = shape[keep];
-  TK_CUDA(cudaMemsetAsync(out, 0, (size_t)nkeep * 8, st));
+  double* out = outs[0];
+  PeerOuts po{};
+  for (int i = 0; i < nout; ++i) po.p[i] = outs[i];
+  po.n = nout;
+  auto zero_owned = [&]() -> int {
+    if (key_hi <= key_lo) return TK_OK;
+    if (nout == 1) {
+      TK_CUDA(cudaMemsetAsync(out + key_lo, 0, (size_t)(key_hi - key_lo) * 8, st));
+    } else {
+      zero_range_kernel<<<(unsigned)std::min<long long>((key_hi - key_lo + 255) / 256, num_sms() * 4), 256, 0, st>>>(
+          po, key_lo, key_hi);
+      count_launch();
+      TK_CUDA(cudaGetLastError());
+    }
+    return TK_OK;
+  };
+  if (int rc = zero_owned()) return rc;
   if (nnz == 0) return TK_OK;
   Counters* hc = static_cast<Counters*>(pinned_scratch(sizeof(Counters)));
   if (keep == 0 && d >= 2) {
@@ -877,6 +926,10 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     }
     p.vals = vals;
     p.out = out;
+    for (int i = 0; i < nout; ++i) p.outs[i] = outs[i];
+    p.nout = nout;
+    p.key_lo = key_lo;
+    p.key_hi = key_hi;
     char* b = scratch.as<char>();
     p.c_first = reinterpret_cast<double*>(b);
     p.c_last = reinterpret_cast<double*>(b + per);
@@ -923,7 +976,7 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     ktimer_begin(st);
     kern<<<(unsigned)blocks, threads, smem, st>>>(p, nspans);
     dense_fixup_kernel<<<(unsigned)((nspans + 255) / 256), 256, 0, st>>>(nspans, p.c_first, p.c_last, p.c_lastkey,
-                                                                         p.c_flags, shape[0], out);
+                                                                         p.c_flags, p);
     ktimer_end(st);
     count_launch(2);
     TK_CUDA(cudaGetLastError());
@@ -932,9 +985,32 @@ int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* co
     if (hc->flags & kFlagIndex) return fail(TK_EINDEX, "ttv: contracted-mode index out of range for its vector");
     if (hc->flags & kFlagKeptOob) return fail(TK_EDIM, "index out of bounds for shape");
     if (!(hc->flags & kFlagUnsorted)) return TK_OK;
-    TK_CUDA(cudaMemsetAsync(out, 0, (size_t)nkeep * 8, st));
   }
-  // chained single-mode TTV on the device, descending modes (the oracle's definition)
+  // general case: the chain of single-mode TTVs; with one output owning every index it writes the
+  // output directly, otherwise a local vector whose owned range is stored into every copy
+  if (nout == 1 && key_lo == 0 && key_hi == nkeep) {
+    TK_CUDA(cudaMemsetAsync(out, 0, (size_t)nkeep * 8, st));  // the fused kernel may have stored some
+    return ttv_dense_chain(d, shape, nnz, cols, vals, keep, vecs, out, st);
+  }
+  DevBuf full;
+  if (int rc = full.alloc((size_t)nkeep * 8, st)) return rc;
+  TK_CUDA(cudaMemsetAsync(full.get(), 0, (size_t)nkeep * 8, st));
+  if (int rc = ttv_dense_chain(d, shape, nnz, cols, vals, keep, vecs, full.as<double>(), st)) return rc;
+  if (key_hi > key_lo) {
+    bcast_range_kernel<<<(unsigned)std::min<long long>((key_hi - key_lo + 255) / 256, num_sms() * 4), 256, 0, st>>>(
+        full.as<double>(), po, key_lo, key_hi);
+    count_launch();
+    TK_CUDA(cudaGetLastError());
+  }
+  TK_CUDA(cudaStreamSynchronize(st));  // `full` is released on return
+  return TK_OK;
+}
+
+// Chained single-mode TTV on the device, descending modes (the oracle's definition), then
+// densify into out (zeroed by the caller).
+int ttv_dense_chain(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    int keep, const double* const* vecs, double* out, cudaStream_t st) {
+  const long long nkeep = shape[keep];
   std::vector<int64_t> cur_shape(shape, shape + d);
   std::vector<const int64_t*> cur_cols(cols, cols + d);
   const double* cur_vals = vals;

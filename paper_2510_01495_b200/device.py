@@ -105,6 +105,18 @@ class DeviceCoo:
         return out
 
 
+    def ttv_dense_peers(self, vecs: dict, keep: int, outs, key_lo: int, key_hi: int, stream=None):
+        """Sharded dense TTV: this shard's result for keep-mode indices [key_lo, key_hi) stored
+        into every output copy in ``outs`` (tensors or raw device pointers: this GPU's vector and
+        peers' vectors mapped with ``ipc_open``) by the kernel itself (tk_ttv_dense_f64_device_peers)."""
+        d = self.ndim
+        ptrs = [0 if m == keep else vecs[m].data_ptr() for m in range(d)]
+        optrs = [o if isinstance(o, int) else o.data_ptr() for o in outs]
+        _lib.check(_lib.load().tk_ttv_dense_f64_device_peers(
+            d, _lib.i64_array(self.shape), self.nnz, _lib.ptr_array([c.data_ptr() for c in self.cols]),
+            self.vals.data_ptr(), int(keep), _lib.ptr_array(ptrs), _lib.ptr_array(optrs), len(optrs),
+            int(key_lo), int(key_hi), _stream_handle(stream)))
+
     def mttkrp(self, factors: dict, n: int, out=None, stream=None):
         """Mode-``n`` MTTKRP with row-major device factors ``{m: (shape[m], R)}``; dense
         float64[(shape[n], R)] (tk_mttkrp_f64_device)."""
@@ -133,3 +145,39 @@ def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor, stream=None) -> Non
 def matvec(a: torch.Tensor, x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     _lib.check(_lib.load().tk_matvec_f64_device(a.data_ptr(), int(a.shape[0]), int(a.shape[1]), x.data_ptr(),
                                                  y.data_ptr(), _stream_handle(stream)))
+
+
+class IpcVector:
+    """A float64 device vector in its own exportable allocation (tk_ipc_alloc), usable as a
+    zero-copy torch tensor (``.tensor``) and exportable to peer processes (``.handle()``)."""
+
+    def __init__(self, n: int, device_index: int):
+        self.n, self.device_index = int(n), int(device_index)
+        p = ctypes.c_void_p()
+        _lib.check(_lib.load().tk_ipc_alloc(max(8 * self.n, 8), ctypes.byref(p)))
+        self.ptr = int(p.value)
+        self.__cuda_array_interface__ = {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device=f"cuda:{self.device_index}")
+
+    def handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _lib.check(_lib.load().tk_ipc_get_handle(self.ptr, h))
+        return h.raw
+
+    def free(self) -> None:
+        if self.ptr:
+            self.tensor = None
+            _lib.check(_lib.load().tk_ipc_free(self.ptr))
+            self.ptr = 0
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer's exported allocation into this process; returns its device pointer."""
+    p = ctypes.c_void_p()
+    _lib.check(_lib.load().tk_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().tk_ipc_close(ctypes.c_void_p(ptr)))

@@ -7,9 +7,13 @@ Nonzeros are independent units; the only exchange is the merge of results (SURVE
 * sparse result (configs 3, 5): every rank's output is a canonical slice and the
   rank-order concatenation IS the canonical result, bitwise equal to one GPU; the merge is
   an all-gather of per-rank counts (global offsets), no data moves;
-* dense result (config 4): each rank writes only the keep-mode rows it owns into a
-  full-length vector (zeros elsewhere) and an all-reduce(sum) merges them -- every element
-  has exactly one non-zero contributor, so the sum is exact.
+* dense result (config 4): each rank owns the keep-mode indices of its shard.  The B200
+  path (``PeerDenseMerge``) has the TTV kernel itself store every owned element -- values,
+  and zeros for indices without rows -- into every rank's output vector, mapped over NVLink
+  by CUDA IPC, so one stream-ordered barrier completes the merge (no all-reduce of the
+  vector).  ``merge_dense`` keeps the all-reduce form (each rank writes only its rows into a
+  zeroed full-length vector; every element has exactly one non-zero contributor, so the sum
+  is exact) as the NCCL baseline.
 
 The host-side logic here is exercised with gloo on CPU (tests/test_multi_cpu.py); on the
 GPU box the same calls run over NCCL.
@@ -77,6 +81,72 @@ def global_offsets(counts) -> list:
     for c in counts:
         off.append(off[-1] + c)
     return off
+
+
+def owned_key_range(key: torch.Tensor, bounds, rank: int, nkeep: int) -> tuple:
+    """Keep-mode indices [lo, hi) rank ``rank`` owns for a dense result: from the key of its first
+    row (0 for rank 0) to the key of the next rank's first row (``nkeep`` for the last rank).
+    ``key`` is the keep-mode column (non-decreasing), ``bounds`` from ``shard_bounds``.  The
+    ranges partition [0, nkeep), so every element of the result has exactly one owner."""
+    n = int(key.shape[0])
+    world = len(bounds) - 1
+
+    def first_key(r):
+        if r == 0:
+            return 0
+        if r >= world or bounds[r] >= n:
+            return nkeep
+        return int(key[bounds[r]].item())
+    lo, hi = first_key(rank), first_key(rank + 1)
+    return lo, max(lo, hi)
+
+
+class PeerDenseMerge:
+    """Sharded dense TTV merged by the kernel's own NVLink stores (stage 2).
+
+    Every rank allocates its output vector in an exportable allocation, the 64-byte CUDA IPC
+    handles are all-gathered once, and each rank maps its peers' vectors.  ``run`` launches
+    ``tk_ttv_dense_f64_device_peers`` with all N output pointers and the rank's owned key range,
+    then a stream-ordered barrier (a one-element all-reduce: it completes only after every
+    rank's kernel, hence every peer store, has finished).  Afterwards every rank's ``out`` holds
+    the full result, identical on all ranks.
+    """
+
+    def __init__(self, nkeep: int, device_index: int):
+        from .device import IpcVector, ipc_open
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.local = IpcVector(nkeep, device_index)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.local.handle())
+        self.ptrs = [self.local.ptr if r == self.rank else ipc_open(h) for r, h in enumerate(handles)]
+        self.device = torch.device(f"cuda:{device_index}")
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    @property
+    def out(self) -> torch.Tensor:
+        return self.local.tensor
+
+    def run(self, dt, vecs: dict, keep: int, key_lo: int, key_hi: int, stream=None) -> torch.Tensor:
+        dt.ttv_dense_peers(vecs, keep, self.ptrs, key_lo, key_hi, stream)
+        self.barrier()
+        return self.out
+
+    def barrier(self):
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(self._flag)  # stream-ordered behind the kernel on every rank
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier()
+
+    def close(self):
+        from .device import ipc_close
+        torch.cuda.synchronize(self.device)
+        dist.barrier()  # nobody stores into a mapping that is going away
+        for r, p in enumerate(self.ptrs):
+            if r != self.rank:
+                ipc_close(p)
+        dist.barrier()
+        self.local.free()
 
 
 def merge_dense(out: torch.Tensor) -> torch.Tensor:

@@ -485,3 +485,101 @@ def test_mttkrp_errors_and_unsorted_input(oracle):
     nz = ref != 0
     assert np.array_equal(got != 0, nz)
     assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= REL
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_dense_peer_stores_merge_shards(oracle, world):
+    """Sharded config-4-shaped dense TTV merged by the kernel's own stores
+    (tk_ttv_dense_f64_device_peers): every shard writes its owned keep-mode range into all
+    `world` output copies; afterwards every copy is identical, equals the chained oracle within
+    1e-12, and carries exact zeros for keep indices without rows.  (One GPU, one process: the
+    copies stand in for the peers' NVLink-mapped vectors; no kernel waits on another.)"""
+    import torch
+    from paper_2510_01495_b200 import multi
+    from paper_2510_01495_b200.device import DeviceCoo
+    shape = (3000, 40, 50, 60)
+    subs, vals = _canonical_coo(shape, 400000, seed=31)
+    keep_rows = subs[:, 0] % 7 != 3  # holes in the keep mode: owned indices without rows
+    subs, vals = subs[keep_rows], vals[keep_rows]
+    t = DeviceCoo.from_host(subs, vals, shape)
+    hv = {m: np.random.default_rng(40 + m).random(shape[m]) + 0.5 for m in (1, 2, 3)}
+    vecs = {m: torch.from_numpy(v).cuda() for m, v in hv.items()}
+    ref = oracle.ttv_multi_dense(subs, vals, shape, hv, 0)
+    outs = [torch.full((shape[0],), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
+    key = t.cols[0]
+    bounds = multi.shard_bounds(key, world)
+    for r in range(world):
+        lo, hi = multi.owned_key_range(key, bounds, r, shape[0])
+        t.slice(bounds[r], bounds[r + 1]).ttv_dense_peers(vecs, 0, outs, lo, hi)
+    torch.cuda.synchronize()
+    got = [o.cpu().numpy() for o in outs]
+    for g in got[1:]:
+        assert g.tobytes() == got[0].tobytes()
+    out = got[0]
+    assert not np.isnan(out).any()
+    assert np.array_equal(out == 0, ref == 0)
+    nz = ref != 0
+    assert np.max(np.abs(out[nz] - ref[nz]) / np.abs(ref[nz])) <= REL
+    # an unsorted shard takes the chained path and still stores only its own range
+    perm = np.random.default_rng(2).permutation(len(vals))
+    u = DeviceCoo.from_host(subs[perm], vals[perm], shape)
+    o2 = [torch.full((shape[0],), -1.0, dtype=torch.float64, device="cuda") for _ in range(2)]
+    u.ttv_dense_peers(vecs, 0, o2, 100, 2000)
+    for o in o2:
+        h = o.cpu().numpy()
+        assert (h[:100] == -1.0).all() and (h[2000:] == -1.0).all()
+        assert h[100:2000].tobytes() == oracle.ttv_multi_dense(subs[perm], vals[perm], shape, hv, 0)[100:2000].tobytes()
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_01495_b200 import multi
+        from paper_2510_01495_b200.device import DeviceCoo
+        torch.cuda.set_device(0)
+        shape = (500, 30, 30, 30)
+        t = DeviceCoo.generate(shape, 300000, seed=77)
+        vecs = {m: torch.rand(shape[m], dtype=torch.float64, device="cuda",
+                              generator=torch.Generator(device="cuda").manual_seed(m)) for m in (1, 2, 3)}
+        full = t.ttv_dense(vecs, 0).cpu().numpy()
+        merge = multi.PeerDenseMerge(shape[0], 0)
+        bounds = multi.shard_bounds(t.cols[0], world)
+        lo, hi = multi.owned_key_range(t.cols[0], bounds, rank, shape[0])
+        out = merge.run(t.slice(bounds[rank], bounds[rank + 1]), vecs, 0, lo, hi).cpu().numpy()
+        merge.close()
+        rel = float(np.max(np.abs(out - full) / np.abs(full)))
+        q.put((rank, rel, lo, hi))
+    except Exception as exc:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(exc), -1, -1))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dense_peer_merge_over_cuda_ipc_two_processes():
+    """PeerDenseMerge end to end: two processes (both on cuda:0 -- one GPU here) export their
+    output vectors by CUDA IPC, map each other's, and each shard's kernel stores its owned range
+    into both; after the barrier both hold the full result (within 1e-12 of one-shot)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, rel, lo, hi in res:
+        assert not isinstance(rel, str), rel
+        assert rel <= REL
+    assert res[0][2] == 0 and res[0][3] == res[1][2] and res[1][3] == 500

@@ -107,3 +107,26 @@ def test_shard_bounds_edge_cases():
     # a single huge group cannot be split: everything lands on one rank
     assert multi.shard_bounds(torch.zeros(8, dtype=torch.int64), 3) == [0, 8, 8, 8]
     assert multi.shard_bounds(torch.zeros(0, dtype=torch.int64), 2) == [0, 0, 0]
+
+
+def test_owned_key_ranges_partition_the_keep_mode():
+    """Dense-result ownership (PeerDenseMerge): the ranks' [lo, hi) ranges tile [0, nkeep) and
+    every key of a shard lies in its own rank's range, including empty shards and keys without
+    rows at either end."""
+    rng = np.random.default_rng(4)
+    for trial in range(40):
+        nkeep = int(rng.integers(1, 30))
+        n = int(rng.integers(0, 200))
+        key = torch.from_numpy(np.sort(rng.integers(0, nkeep, size=n)))
+        for world in (1, 2, 3, 5, 8):
+            bounds = multi.shard_bounds(key, world)
+            ranges = [multi.owned_key_range(key, bounds, r, nkeep) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == nkeep
+            for r in range(world - 1):
+                assert ranges[r][1] == ranges[r + 1][0]
+            for r in range(world):
+                lo, hi = ranges[r]
+                ks = key[bounds[r]:bounds[r + 1]]
+                assert lo <= hi
+                if ks.numel():
+                    assert lo <= int(ks.min()) and int(ks.max()) < hi
