@@ -16,6 +16,8 @@
 //   4. coalesced writes of (key, value) at base + local id; the spilling group last.
 #pragma once
 
+#include <climits>
+
 #include "tk_stream.cuh"
 
 namespace tk {
@@ -52,6 +54,10 @@ constexpr int kTileThreads = TK_TILE_THREADS;  // threads per CTA
 #define TKR(slot)
 #endif
 constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kSpillSlots = 4;  // 128-row chunks of the spill ring (4 KB of the 6.4 KB subk column)
+
+__device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
 // Tile status word: while counting, every warp adds (1 << 56) | its head count (so the aggregate is
 // complete when the warp field reads kTileWarps); the scanner then stores kStPre | inclusive prefix.
 constexpr int kStWarpShift = 56;
@@ -186,6 +192,10 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   __shared__ unsigned int s_head[WORDS];
   __shared__ unsigned long long s_base;
   __shared__ unsigned int s_flags;
+  // spill ring (raw source): warps 1-3 produce 128-row chunks of w past the stage into
+  // kSpillSlots slots of the free subk column, warp 0 folds them in order
+  __shared__ int s_ready[kSpillSlots], s_end[kSpillSlots];
+  __shared__ int s_known, s_last, s_consumed;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long ntiles = (p.n + TILE - 1) / TILE;
@@ -208,6 +218,13 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     const long long tile = fold_tile;
     s_tile = tile;
     s_flags = 0;
+    if constexpr (SRC == kSrcRaw) {
+#pragma unroll
+      for (int i = 0; i < kSpillSlots; ++i) s_ready[i] = 0;
+      s_known = 0;
+      s_last = INT_MAX;
+      s_consumed = 0;
+    }
     const long long start = tile * TILE;
     const long long avail = min((long long)ROWS, p.n - start);
     const bool bulk = p.bulk_ok && avail == ROWS;
@@ -498,7 +515,100 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   zeros = __reduce_add_sync(0xffffffffu, zeros);
   if (lane == 0 && zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
   if (tid == 0) TKR(6);
-  if (warp != 0 || open_li < 0) return;
+  if (open_li < 0) return;
+  if constexpr (SRC == kSrcRaw) {
+    // ---- the group that runs past the halo, raw source: a producer/consumer ring.  Warps 1-3
+    //      (done with their folds) produce chunk c = warp-1, warp+2, ...: 128 rows past the stage
+    //      (L2-hot: the next tiles' CTAs read them), key check, w = val * x[subk] with the gather,
+    //      into slot c % kSpillSlots.  A chunk is loaded only once its predecessor is known to
+    //      continue the group (s_known), and into a slot warp 0 has finished (s_consumed).  Warp
+    //      0's lane 0 folds its in-stage rows, then the slots in chunk order: a pure serial chain,
+    //      the loads and gathers of later chunks in flight meanwhile. ----
+    const int r0 = s_row[open_li];
+    double* ring = reinterpret_cast<double*>(s_subk);
+    constexpr int RW = 4, CH = 32 * RW;
+    if (warp != 0) {
+      long long gk[NKR];
+#pragma unroll
+      for (int c = 0; c < NKR; ++c)
+        if (NK > 0 || c < nk) gk[c] = s_key[c * ROWS + r0];
+      for (int c = warp - 1;; c += kTileWarps - 1) {
+        int go = 1;
+        if (lane == 0) {
+          while (true) {  // predecessor known to continue, and this chunk's slot consumed
+            if (c > ld_vol(&s_last)) {
+              go = 0;
+              break;
+            }
+            if (ld_vol(&s_known) >= c && ld_vol(&s_consumed) >= c - kSpillSlots + 1) break;
+            __nanosleep(32);
+          }
+        }
+        if (!__shfl_sync(0xffffffffu, go, 0)) return;
+        const long long pos = start + avail + (long long)c * CH;
+        long long kv[RW][NKR], sk[RW];
+        double av[RW];
+#pragma unroll
+        for (int j = 0; j < RW; ++j) {  // every load of the chunk in flight at once
+          const long long row = pos + j * 32 + lane;
+          const bool ok = row < p.n;
+#pragma unroll
+          for (int q = 0; q < NKR; ++q)
+            if (NK > 0 || q < nk) kv[j][q] = ok ? __ldcg(p.key[q] + row) : 0;
+          av[j] = ok ? __ldcg(p.a + row) : 0.0;
+          sk[j] = ok ? __ldcg(p.subk + row) : 0;
+        }
+        int end = CH;
+        double xv[RW];
+#pragma unroll
+        for (int j = 0; j < RW; ++j) {
+          bool same = pos + j * 32 + lane < p.n;
+#pragma unroll
+          for (int q = 0; q < NKR; ++q)
+            if (NK > 0 || q < nk) same = same && kv[j][q] == gk[q];
+          const unsigned int m = __ballot_sync(0xffffffffu, !same);
+          if (end == CH && m) end = j * 32 + __ffs(m) - 1;
+          xv[j] = (unsigned long long)sk[j] < (unsigned long long)p.nx ? __ldg(p.x + sk[j]) : 0.0;
+        }
+        const bool last = end < CH || pos + CH >= p.n;
+        if (lane == 0) {  // the next chunk may start loading now (or nothing past this one is needed)
+          if (last) st_vol(&s_last, c);
+          else st_vol(&s_known, c + 1);
+        }
+        double* slot = ring + (c % kSpillSlots) * CH;
+#pragma unroll
+        for (int j = 0; j < RW; ++j) slot[j * 32 + lane] = __dmul_rn(av[j], xv[j]);
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) {
+          st_vol(&s_end[c % kSpillSlots], end);
+          __threadfence_block();
+          st_vol(&s_ready[c % kSpillSlots], c + 1);
+        }
+        if (last) return;
+      }
+    }
+    if (lane != 0) return;
+    double acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
+    for (int c = 0;; ++c) {
+      const int sl = c % kSpillSlots;
+      while (ld_vol(&s_ready[sl]) != c + 1) __nanosleep(16);
+      __threadfence_block();
+      const int end = ld_vol(&s_end[sl]);
+      acc = fold_run(ring + sl * CH, 0, end, acc);
+      __threadfence_block();
+      st_vol(&s_consumed, c + 1);
+      if (c == ld_vol(&s_last)) break;
+    }
+    long long k[NKR];
+#pragma unroll
+    for (int c = 0; c < NKR; ++c)
+      if (NK > 0 || c < nk) k[c] = s_key[c * ROWS + r0];
+    seg_emit<SRC>(p, base + open_li, k, acc);
+    TKR(7);
+    return;
+  }
+  if (warp != 0) return;
 
   // ---- the group that runs past the halo, finished by warp 0 alone: 128-row chunks (L2-hot: the
   //      next tiles' CTAs read them), w staged in the free subk column; the next chunk's loads are
