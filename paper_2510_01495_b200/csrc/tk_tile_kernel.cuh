@@ -54,7 +54,16 @@ constexpr int kTileThreads = TK_TILE_THREADS;  // threads per CTA
 #define TKR(slot)
 #endif
 constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kSpillSlots = 4;  // 128-row chunks of the spill ring (4 KB of the 6.4 KB subk column)
+#ifndef TK_SPILL_SLOTS
+#define TK_SPILL_SLOTS 6
+#endif
+#ifndef TK_RING_WATCHDOG
+#define TK_RING_WATCHDOG 0  // spin limits on the CTA-local spill ring (costs ~3% at cfg5; debug)
+#endif
+#ifndef TK_SPILL_W0FIRST
+#define TK_SPILL_W0FIRST 0  // with an open group, warp 0 skips the striped folds (measured slower)
+#endif
+constexpr int kSpillSlots = TK_SPILL_SLOTS;  // 128-row chunks of the spill ring (in the 6.4 KB subk column)
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
@@ -504,7 +513,12 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   //      on -- every thread knows that without a barrier. ----
   const int open_li = (agg > 0 && agg == ptot && start + avail < p.n) ? agg - 1 : -1;
   unsigned int zeros = 0;
-  for (int li = tid; li < agg; li += kTileThreads) {
+  // with an open group (raw source) warp 0 starts its serial chain at once: warps 1-3 take the
+  // striped folds (then produce the spill chunks)
+  const bool w0_chain = TK_SPILL_W0FIRST && SRC == kSrcRaw && open_li >= 0;
+  const int li0 = w0_chain ? (warp == 0 ? agg : tid - 32) : tid;
+  const int lstep = w0_chain ? kTileThreads - 32 : kTileThreads;
+  for (int li = li0; li < agg; li += lstep) {
     if (li == open_li) continue;
     const int r = s_row[li];
     const int end = li + 1 < ptot ? s_row[li + 1] : avail;
@@ -534,13 +548,24 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
         if (NK > 0 || c < nk) gk[c] = s_key[c * ROWS + r0];
       for (int c = warp - 1;; c += kTileWarps - 1) {
         int go = 1;
+        [[maybe_unused]] unsigned int spins = 0;
         if (lane == 0) {
           while (true) {  // predecessor known to continue, and this chunk's slot consumed
             if (c > ld_vol(&s_last)) {
               go = 0;
               break;
             }
+            // (a chunk must not start before its predecessor is known to continue: a chunk past
+            // the group's end would otherwise also report itself last)
             if (ld_vol(&s_known) >= c && ld_vol(&s_consumed) >= c - kSpillSlots + 1) break;
+#if TK_RING_WATCHDOG
+            if (++spins == kSpinLimit) {
+              tile_stall(p.ctr, 5, tile);
+              st_vol(&s_last, -1);  // the consumer gives up too
+              go = 0;
+              break;
+            }
+#endif
             __nanosleep(32);
           }
         }
@@ -592,7 +617,16 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
     double acc = fold_run(s_a, r0 + 1, avail, s_a[r0]);
     for (int c = 0;; ++c) {
       const int sl = c % kSpillSlots;
-      while (ld_vol(&s_ready[sl]) != c + 1) __nanosleep(16);
+      [[maybe_unused]] unsigned int spins = 0;
+      while (ld_vol(&s_ready[sl]) != c + 1) {
+#if TK_RING_WATCHDOG
+        if (ld_vol(&s_last) < 0 || ++spins == kSpinLimit) {  // a producer gave up: the call fails
+          tile_stall(p.ctr, 6, tile);
+          return;
+        }
+#endif
+        __nanosleep(16);
+      }
       __threadfence_block();
       const int end = ld_vol(&s_end[sl]);
       acc = fold_run(ring + sl * CH, 0, end, acc);
