@@ -60,6 +60,9 @@ constexpr int kTileWarps = kTileThreads / 32;
 #ifndef TK_RING_WATCHDOG
 #define TK_RING_WATCHDOG 0  // spin limits on the CTA-local spill ring (costs ~3% at cfg5; debug)
 #endif
+#ifndef TK_SPILL_AHEAD
+#define TK_SPILL_AHEAD 1  // spill chunks loaded ahead of the last one known to continue the group (2, 3: slower)
+#endif
 #ifndef TK_SPILL_W0FIRST
 #define TK_SPILL_W0FIRST 0  // with an open group, warp 0 skips the striped folds (measured slower)
 #endif
@@ -555,9 +558,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
               go = 0;
               break;
             }
-            // (a chunk must not start before its predecessor is known to continue: a chunk past
-            // the group's end would otherwise also report itself last)
-            if (ld_vol(&s_known) >= c && ld_vol(&s_consumed) >= c - kSpillSlots + 1) break;
+            // up to TK_SPILL_AHEAD chunks past the last one known to continue the group are
+            // loaded speculatively (wasted L2 reads when the group ends sooner)
+            if (ld_vol(&s_known) >= c - TK_SPILL_AHEAD + 1 && ld_vol(&s_consumed) >= c - kSpillSlots + 1) break;
 #if TK_RING_WATCHDOG
             if (++spins == kSpinLimit) {
               tile_stall(p.ctr, 5, tile);
@@ -596,9 +599,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
           xv[j] = (unsigned long long)sk[j] < (unsigned long long)p.nx ? __ldg(p.x + sk[j]) : 0.0;
         }
         const bool last = end < CH || pos + CH >= p.n;
-        if (lane == 0) {  // the next chunk may start loading now (or nothing past this one is needed)
-          if (last) st_vol(&s_last, c);
-          else st_vol(&s_known, c + 1);
+        if (lane == 0) {  // later chunks may start loading (or nothing past this one is needed)
+          if (last) atomicMin(&s_last, c);
+          else atomicMax(&s_known, c + 1);
         }
         double* slot = ring + (c % kSpillSlots) * CH;
 #pragma unroll
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       acc = fold_run(ring + sl * CH, 0, end, acc);
       __threadfence_block();
       st_vol(&s_consumed, c + 1);
-      if (c == ld_vol(&s_last)) break;
+      if (end < CH || start + avail + (long long)(c + 1) * CH >= p.n) break;  // the group ended here
     }
     long long k[NKR];
 #pragma unroll
