@@ -569,9 +569,6 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
 #ifndef TK_TILE_LAG
 #define TK_TILE_LAG 1024  // tiles between a tile's count and its fold
 #endif
-#ifndef TK_TILE_LAG_DIV
-#define TK_TILE_LAG_DIV 1
-#endif
 #ifndef TK_TILE_ROWS
 #define TK_TILE_ROWS 768
 #endif
@@ -602,9 +599,7 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
 #endif
   ktimer_begin(st);
   // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
-  // lag: ~TK_TILE_LAG tiles at scale; a small stream keeps it to a fraction of its tiles, so its
-  // folds start within the first wave of CTAs
-  p.lag = std::min<long long>(TK_TILE_LAG, std::max<long long>(32, ntiles / TK_TILE_LAG_DIV));
+  p.lag = std::min<long long>(TK_TILE_LAG, ntiles);
   p.out_v2 = p.out_nk == 2 && aligned16(p.out_subs);
   kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
   ktimer_end(st);
