@@ -533,6 +533,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   if (lane == 0 && zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
   if (tid == 0) TKR(6);
   if (open_li < 0) return;
+#ifdef TK_DIAG_NOSPILL  // diagnostics only: the open group is never finished (wrong output)
+  return;
+#endif
   if constexpr (SRC == kSrcRaw) {
     // ---- the group that runs past the halo, raw source: a producer/consumer ring.  Warps 1-3
     //      (done with their folds) produce chunk c = warp-1, warp+2, ...: 128 rows past the stage
