@@ -152,6 +152,32 @@ def test_single_group_spanning_many_tiles(K, oracle):
     assert_ttv_equal(K.ttv_raw(subs, vals, shape, x, 2), oracle.ttv_raw(subs, vals, shape, x, 2))
 
 
+@pytest.mark.parametrize("tail", ["stream_goes_on", "stream_ends"])
+def test_spill_ring_chunk_boundaries(K, oracle, tail):
+    """The open group's spill ring (128-row chunks past the 768+32-row stage, 6 slots, warps 1-3
+    producing, warp 0 folding): the group headed at row 700 of tile 0 ends exactly at, one
+    before and one after every chunk boundary up to 9 chunks past the stage (wrapping the ring
+    once), with the stream going on afterwards or ending with the group."""
+    stage = 768 + 32
+    for k in range(0, 10):
+        for delta in (-1, 0, 1):
+            end = stage + 128 * k + delta  # first row after the open group
+            if end <= 700:
+                continue
+            lens = [700, end - 700]
+            if tail == "stream_goes_on":
+                lens += [1, 3, 130, 2, 900]
+            lens = np.array(lens)
+            i0 = np.repeat(np.arange(lens.size), lens)
+            i2 = np.concatenate([np.arange(L) for L in lens])
+            subs = np.column_stack([i0, np.zeros_like(i0), i2]).astype(np.int64)
+            vals = np.random.default_rng(k * 7 + delta + 2).standard_normal(i0.size)
+            shape = (lens.size, 1, int(lens.max()))
+            x = np.random.default_rng(k + 40).standard_normal(shape[2])
+            assert_ttv_equal(K.ttv_raw(subs, vals, shape, x, 2), oracle.ttv_raw(subs, vals, shape, x, 2),
+                             f"k={k} delta={delta} {tail}")
+
+
 def test_exact_zero_groups_compacted(K, oracle):
     # +v / -v pairs in the same group cancel exactly; scattered through many tiles
     rng = np.random.default_rng(21)
