@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "dot", "matvec"])
+    ap.add_argument("--what", default="cfg5", choices=["cfg5", "cfg5k1", "cfg4", "cfg3", "dot", "matvec"])
     ap.add_argument("--nnz", type=int, default=100_000_000)
     ap.add_argument("--iters", type=int, default=3)
     a = ap.parse_args()
@@ -22,7 +22,16 @@ def main():
     from paper_2510_01495_b200 import synth
     from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
     torch.cuda.set_device(0)
-    if a.what == "cfg5":
+    if a.what == "cfg5k1":  # the middle mode: the general (sort) path
+        shape = (10**6, 10**5, 10**4)
+        t = DeviceCoo.generate(shape, a.nnz, zipf_s=1.2, normal_vals=True, seed=12345)
+        x = uniform_vector(shape[1], 778)
+        os_ = torch.empty((t.nnz, 2), dtype=torch.int64, device="cuda")
+        ov = torch.empty(t.nnz, dtype=torch.float64, device="cuda")
+        for _ in range(a.iters):
+            u, _, _ = t.ttv(x, 1, os_, ov)
+        print("cfg5k1 u", u)
+    elif a.what == "cfg5":
         shape = (10**6, 10**5, 10**4)
         t = DeviceCoo.generate(shape, a.nnz, zipf_s=1.2, normal_vals=True, seed=12345)
         x = uniform_vector(shape[2], 777)
