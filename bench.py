@@ -58,9 +58,24 @@ class ClockSampler:
         self._thr = None
         self._nv = None
 
+    def _handle(self):
+        """NVML handle of CUDA device `index`, matched by PCI bus id (NVML and CUDA orders can
+        differ, e.g. under CUDA_VISIBLE_DEVICES), else by index."""
+        nv = self._nv
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
     def _loop(self):
         nv = self._nv
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        try:
+            h = self._handle()
+        except Exception:  # noqa: BLE001 - sampling must never break the bench
+            return
         names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                  "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                  "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
@@ -109,8 +124,15 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # TK_BENCH_ONE_GPU=1 + TK_BENCH_BACKEND=gloo: path check only -- every rank on device 0,
+        # collectives on the host (no kernel waits on another rank); never a measurement
+        dev = 0 if os.environ.get("TK_BENCH_ONE_GPU") == "1" else local
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("TK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -122,12 +144,19 @@ def barrier(world):
         dist.barrier()
 
 
+def coll_device():
+    """Where collective operands live: the GPU under NCCL, the host under gloo."""
+    import torch
+    import torch.distributed as dist
+    return torch.device("cuda") if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
 def max_over_ranks(v: float, world: int) -> float:
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -375,7 +404,10 @@ def multi_dense_measurement(rank, world, steps, warmup):
 
     def nccl_step():
         t.ttv_dense(vecs, 0, red)
-        dist.all_reduce(red)
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(red)
+        else:  # path check under gloo: the same sum through the host
+            red.copy_(multi.merge_dense(red.cpu()))
 
     res = {}
     for name, fn in (("kernel_store_merge", peer_step), ("nccl_allreduce_merge", nccl_step)):
@@ -432,7 +464,7 @@ def run_ours(args):
     def step():
         u, _, _ = t.ttv(x, k, out_subs, out_vals)
         if world > 1:
-            counts = multi.gather_counts(u, torch.device("cuda"))
+            counts = multi.gather_counts(u, coll_device())
             return u, counts
         return u, [u]
 
@@ -446,7 +478,7 @@ def run_ours(args):
     barrier(world)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(torch.cuda.current_device()) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
             u_local, counts = step()
