@@ -63,6 +63,9 @@ constexpr int kTileWarps = kTileThreads / 32;
 #ifndef TK_SPILL_AHEAD
 #define TK_SPILL_AHEAD 1  // spill chunks loaded ahead of the last one known to continue the group (2, 3: slower)
 #endif
+#ifndef TK_SPILL_NAP
+#define TK_SPILL_NAP 32  // ns between a waiting producer's polls
+#endif
 #ifndef TK_SPILL_W0FIRST
 #define TK_SPILL_W0FIRST 0  // with an open group, warp 0 skips the striped folds (measured slower)
 #endif
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
               break;
             }
 #endif
-            __nanosleep(32);
+            __nanosleep(TK_SPILL_NAP);
           }
         }
         if (!__shfl_sync(0xffffffffu, go, 0)) return;
