@@ -72,10 +72,7 @@ class ClockSampler:
 
     def _loop(self):
         nv = self._nv
-        try:
-            h = self._handle()
-        except Exception:  # noqa: BLE001 - sampling must never break the bench
-            return
+        h = self._h
         names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                  "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                  "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
@@ -95,6 +92,7 @@ class ClockSampler:
             import pynvml as nv
             nv.nvmlInit()
             self._nv = nv
+            self._h = self._handle()  # resolved before the timed region starts
             self._thr = threading.Thread(target=self._loop, daemon=True)
             self._thr.start()
             time.sleep(0.01)

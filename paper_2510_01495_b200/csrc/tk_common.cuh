@@ -3,7 +3,7 @@
 // Everything on the TTV/dot/matvec path is an FP64, HBM-bandwidth-bound stream
 // (<= 0.125 FLOP/B), so the helpers here are about moving bytes: 1-D TMA bulk
 // copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier, relaxed
-// GPU-scope loads/stores for the decoupled look-back, and a streaming L2
+// GPU-scope loads/stores for the tile prefix scan, and a streaming L2
 // policy for data that is read exactly once.
 #pragma once
 
@@ -95,41 +95,10 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return __ldcs(p);
 }
 
-// ---- decoupled look-back over per-tile counts ----------------------------------------------
+// ---- per-tile status words of the tile kernel's prefix scan -------------------------------------
 // status word: [63:62] = 0 invalid, 1 aggregate, 2 inclusive prefix; [61:0] = count.
 constexpr unsigned long long kStAgg = 1ull << 62;
 constexpr unsigned long long kStPre = 2ull << 62;
 constexpr unsigned long long kStVal = (1ull << 62) - 1;
-
-// Called by one full warp.  Publishes `agg` for `tile` and returns the exclusive prefix
-// (sum of the aggregates of all tiles < tile).  Tiles are handed out in launch order by
-// Counters::tile_ticket, so every predecessor is resident or finished (forward progress).
-__device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long long* status, long long tile,
-                                                                 unsigned long long agg) {
-  const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(status, kStPre | agg);
-    return 0;
-  }
-  if (lane == 0) st_relaxed(status + tile, kStAgg | agg);
-  unsigned long long excl = 0;
-  long long look = tile - 1;
-  while (true) {
-    long long t = look - lane;
-    unsigned long long s = t >= 0 ? ld_relaxed(status + t) : kStPre;
-    while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
-      if ((s >> 62) == 0) s = ld_relaxed(status + t);
-    }
-    unsigned int pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-    unsigned long long v = (pre && lane > __ffs(pre) - 1) ? 0ull : (s & kStVal);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (pre) break;
-    look -= 32;
-  }
-  if (lane == 0) st_relaxed(status + tile, kStPre | (excl + agg));
-  return excl;
-}
 
 }  // namespace tk

@@ -1,24 +1,23 @@
-// tk_tile_kernel.cuh -- sparse-result TTV: one compact CTA per tile, many CTAs per SM.
+// tk_tile_kernel.cuh -- sparse-result TTV: one compact CTA per tile, eight CTAs per SM.
 //
-// Per CTA (256 threads, TILE rows + HALO look-ahead rows, tiles handed out in launch order):
-//   1. thread 0 takes a ticket and stages every column of the tile into shared memory with 1-D
-//      TMA bulk copies (cp.async.bulk, one mbarrier); partial tail tiles use plain loads;
-//   2. w = vals * x[subk] with all gathers in flight before any store (x stays L1-resident: the
-//      CTA needs ~37 KB of shared memory, so four CTAs per SM still leave L1 ~100 KB), and the
-//      head bitmask of the kept-key stream;
-//   3. warp 0: popcount prefix, publish the tile aggregate, decoupled look-back (its latency
-//      overlaps the folds of warps 1-7, and other CTAs on the SM keep the memory pipe busy);
-//      warps 1-7: every group headed in the tile is classified -- short groups are folded at once,
-//      other groups that close inside tile+halo are folded one group per thread from a packed
-//      list, the (at most one) group that runs past the halo is finished cooperatively at the end;
-//      every fold is serial in row order with __dadd_rn: the reference's exact operation sequence
-//      (_ckernels.pyx:274-294), hence bit-identical values;
-//   4. coalesced writes of (key, value) at base + local id; the spilling group last.
+// Per CTA (128 threads, a 768-row tile + 32 halo rows; block b counts tile b-1 and folds tile
+// b-1-lag, block 0 is the sequential prefix scanner):
+//   1. thread 0 stages every column of the fold tile into shared memory with 1-D TMA bulk
+//      copies (cp.async.bulk, one mbarrier); meanwhile every warp counts the group heads of the
+//      count tile straight from global memory and publishes the tile aggregate;
+//   2. head bitmask + order check of the staged keys, popcount prefix, each head row recorded
+//      at its local id; the tile's exclusive prefix (published ~lag tiles earlier by the scanner);
+//   3. w = vals * x[subk] with every gather in flight before any store;
+//   4. every group closing inside the stage is folded by one thread, striped, and written at
+//      base + local id; the group that runs past the stage is finished through the spill ring
+//      (warps 1-3 produce 128-row chunks, warp 0 lane 0 folds).  Every fold is serial in row order
+//      with __dadd_rn: the reference's exact operation sequence (_ckernels.pyx:274-294), hence
+//      bit-identical values.
 #pragma once
 
 #include <climits>
 
-#include "tk_stream.cuh"
+#include "tk_fold.cuh"
 
 namespace tk {
 

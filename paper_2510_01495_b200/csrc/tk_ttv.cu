@@ -2,7 +2,7 @@
 //
 // Paths:
 //   fast    : contracted mode is the trailing mode of a canonical tensor -> the kept
-//             tuples are already sorted; one fused streaming kernel (seg_ttv_kernel<Raw>).
+//             tuples are already sorted; one fused streaming kernel (ttv_tile_kernel<Raw>).
 //   general : any other mode / unsorted input -> w and a linearised kept key per row,
 //             stable device radix sort of (key, w), then the same segmented kernel
 //             (<LinKey>).  Garbage kept indices or keys wider than 62 bits: LSD radix
