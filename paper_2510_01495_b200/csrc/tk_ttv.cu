@@ -14,6 +14,7 @@
 //             ordered fix-up for runs that cross tiles; chained single-mode TTV otherwise.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -56,6 +57,76 @@ __global__ void prep_linkey_kernel2(long long n, int nk, KeepCols kc, const long
     w[r] = wr;
   }
   if (flags) atomicOr(&ctr->flags, flags);
+}
+
+// ---- general path, split by the leading kept mode (canonical input, contracted mode != 0) ----
+// Row offsets of every leading-mode value: off[v] = first row with col0 >= v (off[n0] = n).  Flags
+// kFlagUnsorted if col0 decreases and kFlagKeptOob if it leaves [0, n0): the split is then off.
+__global__ void lead_offsets_kernel(long long n, const long long* __restrict__ col0, long long n0,
+                                    long long* __restrict__ off, Counters* ctr) {
+  unsigned int flags = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= n; r += (long long)gridDim.x * blockDim.x) {
+    const long long prev = r == 0 ? -1 : col0[r - 1];
+    const long long cur = r == n ? n0 : col0[r];
+    if (r < n && (cur < 0 || cur >= n0)) {
+      flags |= kFlagKeptOob;
+      continue;
+    }
+    if (cur < prev) {
+      flags |= kFlagUnsorted;
+      continue;
+    }
+    for (long long v = prev + 1; v <= cur && v <= n0; ++v) off[v] = r;
+  }
+  if (flags) atomicOr(&ctr->flags, flags);
+}
+
+// Split parts: leading-mode interval [lo[j], lo[j+1]) sorted on its own with 32-bit keys.
+constexpr int kMaxParts = 64;
+struct PartTable {
+  long long lo[kMaxParts + 1];  // leading-mode value where each part starts
+  int nparts;
+};
+
+// w = vals * x[subk] and the 32-bit part-local key (lead - lo[part]) * R + rest, where rest is the
+// row-major linearisation of the other kept modes (R = product of their dims).
+__global__ void prep_key32_kernel(long long n, int nk, KeepCols kc, const long long* __restrict__ subk,
+                                  const double* __restrict__ vals, const double* __restrict__ x, long long nx,
+                                  PartTable pt, unsigned int* __restrict__ key, double* __restrict__ w,
+                                  Counters* ctr) {
+  unsigned int flags = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const long long idx = subk[r];
+    double wr = 0.0;
+    if (idx < 0 || idx >= nx) flags |= kFlagIndex;
+    else wr = __dmul_rn(vals[r], __ldg(x + idx));
+    const long long lead = kc.col[0][r];
+    int lo = 0, hi = pt.nparts - 1;  // the part holding `lead` (lead is in range: checked by the offsets)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pt.lo[mid] <= lead) lo = mid;
+      else hi = mid - 1;
+    }
+    long long rest = 0, R = 1;
+    for (int c = 1; c < nk; ++c) {
+      const long long v = kc.col[c][r];
+      if (v < 0 || v >= kc.dims[c]) flags |= kFlagKeptOob;
+      rest = rest * kc.dims[c] + v;
+      R *= kc.dims[c];
+    }
+    key[r] = (unsigned int)((lead - pt.lo[lo]) * R + rest);
+    w[r] = wr;
+  }
+  if (flags) atomicOr(&ctr->flags, flags);
+}
+
+// Back to the global linear key (lin = base + key32) and the sorted w into the tile kernel's input.
+__global__ void widen_part_kernel(long long n, const unsigned int* __restrict__ k32, const double* __restrict__ ws,
+                                  long long base, long long* __restrict__ key, double* __restrict__ w) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    key[r] = base + (long long)k32[r];
+    if (ws != w) w[r] = ws[r];
+  }
 }
 
 __global__ void iota_kernel(long long n, long long* out) {
@@ -566,6 +637,9 @@ int grid_for(long long n, int per_thread = 4) {
 template <int SRC, int NK>
 int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   // one CTA per tile, eight CTAs per SM (~19 KB shared memory each: L1 keeps x resident)
+#ifndef TK_SPLIT_SORT
+#define TK_SPLIT_SORT 1  // general path: per-interval 32-bit sorts when the leading kept mode is sorted
+#endif
 #ifndef TK_TILE_LAG
 #define TK_TILE_LAG 1024  // tiles between a tile's count and its fold
 #endif
@@ -695,6 +769,124 @@ int lin_bits(const std::vector<long long>& dims) {
   return std::max(bits, 1);
 }
 
+constexpr int kDeclined = -1;  // the split path does not apply: take the one-sort path
+
+long long kSplitMinNnz() {  // TK_SPLIT_MIN_NNZ: smallest stream the split path takes (tests lower it)
+  static const long long v = [] {
+    const char* e = getenv("TK_SPLIT_MIN_NNZ");
+    return e ? std::max(1LL, atoll(e)) : (1LL << 22);
+  }();
+  return v;
+}
+
+// General path for canonical input with a non-leading contracted mode (the paper's middle-mode
+// protocol): the rows are already sorted by the leading kept mode, so they are cut into a few
+// leading-mode intervals and each is sorted on its own with 32-bit keys (lead - lo) * R + rest --
+// 8-bit digit passes = ceil(bits / 8), where one global sort needs ceil(log2(n0 * R) / 8) passes of
+// 16-byte (key, w) pairs.  Dense leading values (the Zipf head) get narrow intervals and 2-3
+// passes; the sparse tail wide ones and 4.  Stable sorts in disjoint, ordered intervals give the
+// same order as the one global stable sort, so results stay bit-identical.
+int ttv_general_split(long long nnz, int nk, const KeepCols& kc, const std::vector<long long>& dims,
+                      const int64_t* const* cols, const double* vals, const double* x, long long nx, int k,
+                      int64_t* out_subs, double* out_vals, int64_t* out_nnz, cudaStream_t st, bool keep_zeros) {
+  const long long n0 = dims[0];
+  long long R = 1;
+  for (int c = 1; c < nk; ++c) R *= dims[c];
+  if (nnz < kSplitMinNnz() || n0 > (1LL << 22) || R > (1LL << 31)) return kDeclined;
+  Counters* hc = static_cast<Counters*>(pinned_scratch(sizeof(Counters)));
+  const int g = grid_for(nnz);
+  DevBuf ctrbuf, offb;
+  if (int rc = ctrbuf.alloc(sizeof(Counters), st)) return rc;
+  Counters* dctr = ctrbuf.as<Counters>();
+  TK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(Counters), st));
+  if (int rc = offb.alloc((size_t)(n0 + 1) * 8, st)) return rc;
+  lead_offsets_kernel<<<g, 256, 0, st>>>(nnz, kc.col[0], n0, offb.as<long long>(), dctr);
+  count_launch();
+  TK_CUDA(cudaGetLastError());
+  std::vector<long long> off((size_t)n0 + 1);
+  TK_CUDA(cudaMemcpyAsync(off.data(), offb.get(), (size_t)(n0 + 1) * 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaMemcpyAsync(hc, dctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (hc->flags) return kDeclined;  // unsorted or out-of-range leading column
+
+  // parts: at each start, the fewest digit passes whose interval holds >= kMinRows rows (or
+  // reaches the end); otherwise four passes over the widest 32-bit interval
+  static const long long kMinRows = [] {  // TK_SPLIT_MIN_ROWS: tests force many small intervals
+    const char* e = getenv("TK_SPLIT_MIN_ROWS");
+    return e ? std::max(1LL, atoll(e)) : (1LL << 22);
+  }();
+  PartTable pt{};
+  std::vector<int> pbits;
+  long long a = 0;
+  while (a < n0) {
+    long long b = -1;
+    for (int P = 1; P <= 4 && b < 0; ++P) {
+      const long long W = (1LL << (8 * P)) / R;  // keys (b - a) * R - 1 < 2^(8P)
+      if (W < 1) continue;
+      const long long e = std::min(n0, a + W);
+      if (P == 4 || e == n0 || off[e] - off[a] >= kMinRows) b = e;
+    }
+    if (b <= a || pt.nparts == kMaxParts) return kDeclined;
+    pt.lo[pt.nparts++] = a;
+    const unsigned long long maxkey = (unsigned long long)((b - a) * R - 1);
+    int bits = 1;
+    while (bits < 32 && (maxkey >> bits)) ++bits;
+    pbits.push_back(bits);
+    a = b;
+  }
+  pt.lo[pt.nparts] = n0;
+
+  DevBuf k32a, k32b, wa, wb, keys, temp;
+  if (int rc = k32a.alloc(nnz * 4, st)) return rc;
+  if (int rc = k32b.alloc(nnz * 4, st)) return rc;
+  if (int rc = wa.alloc(nnz * 8, st)) return rc;
+  if (int rc = wb.alloc(nnz * 8, st)) return rc;
+  if (int rc = keys.alloc(nnz * 8, st)) return rc;
+  prep_key32_kernel<<<g, 256, 0, st>>>(nnz, nk, kc, reinterpret_cast<const long long*>(cols[k]), vals, x, nx, pt,
+                                       k32a.as<unsigned int>(), wa.as<double>(), dctr);
+  count_launch();
+  TK_CUDA(cudaGetLastError());
+  TK_CUDA(cudaMemcpyAsync(hc, dctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (hc->flags & kFlagIndex) return finish(*hc, k, nx, nk, nullptr, nullptr, out_nnz, st);
+  if (hc->flags & kFlagKeptOob) return kDeclined;  // garbage kept indices: the LSD path
+
+  size_t tb = 0;
+  long long maxrows = 0;
+  for (int j = 0; j < pt.nparts; ++j) maxrows = std::max(maxrows, off[pt.lo[j + 1]] - off[pt.lo[j]]);
+  {
+    cub::DoubleBuffer<unsigned int> kb(k32a.as<unsigned int>(), k32b.as<unsigned int>());
+    cub::DoubleBuffer<double> vb(wa.as<double>(), wb.as<double>());
+    TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)std::max(maxrows, 1LL), 0, 32, st));
+  }
+  if (int rc = temp.alloc(tb, st)) return rc;
+  for (int j = 0; j < pt.nparts; ++j) {
+    const long long r0 = off[pt.lo[j]], rows = off[pt.lo[j + 1]] - r0;
+    if (rows == 0) continue;
+    cub::DoubleBuffer<unsigned int> kb(k32a.as<unsigned int>() + r0, k32b.as<unsigned int>() + r0);
+    cub::DoubleBuffer<double> vb(wa.as<double>() + r0, wb.as<double>() + r0);
+    size_t tbj = tb;
+    TK_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbj, kb, vb, (int)rows, 0, pbits[j], st));
+    widen_part_kernel<<<grid_for(rows), 256, 0, st>>>(rows, kb.Current(), vb.Current(), pt.lo[j] * R,
+                                                      keys.as<long long>() + r0, wa.as<double>() + r0);
+    count_launch();
+    TK_CUDA(cudaGetLastError());
+  }
+  SegParams p{};
+  p.n = nnz;
+  p.nk = 1;
+  p.key[0] = keys.as<long long>();
+  p.a = wa.as<double>();
+  p.out_nk = nk;
+  for (int c = 0; c < nk; ++c) p.dims[c] = dims[c];
+  p.out_subs = reinterpret_cast<long long*>(out_subs);
+  p.out_vals = out_vals;
+  p.bulk_ok = aligned16(p.key[0]) && aligned16(p.a);
+  Counters res{};
+  if (int rc = run_seg(kSrcLinKey, p, st, &res)) return rc;
+  return finish(res, k, nx, nk, p.out_subs, out_vals, out_nnz, st, keep_zeros);
+}
+
 int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const* cols, const double* vals,
                 const double* x, long long nx, int k, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
                 cudaStream_t st, bool keep_zeros) {
@@ -722,6 +914,16 @@ int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const
   if (int rc = w2.alloc(nnz * 8, st)) return rc;
 
   bool linear = bits > 0;
+  // TK_SPLIT_SORT=0 in the environment forces the one-sort path (parity tests compare the two)
+  static const bool split_env_off = [] {
+    const char* e = getenv("TK_SPLIT_SORT");
+    return e && e[0] == '0';
+  }();
+  if (linear && k != 0 && TK_SPLIT_SORT && !split_env_off) {
+    const int rc = ttv_general_split(nnz, nk, kc, dims, cols, vals, x, nx, k, out_subs, out_vals, out_nnz, st,
+                                     keep_zeros);
+    if (rc != kDeclined) return rc;
+  }
   if (linear) {
     prep_linkey_kernel2<<<g, 256, 0, st>>>(nnz, nk, kc, reinterpret_cast<const long long*>(cols[k]), vals, x, nx,
                                            keys.as<long long>(), w.as<double>(), dctr);

@@ -609,3 +609,75 @@ def test_dense_peer_merge_over_cuda_ipc_two_processes():
         assert not isinstance(rel, str), rel
         assert rel <= REL
     assert res[0][2] == 0 and res[0][3] == res[1][2] and res[1][3] == 500
+
+
+def _split_case(queue, env):
+    import os
+    os.environ.update(env)
+    from oracle import oracle
+    from paper_2510_01495_b200 import backend
+    K = backend.kernels()
+    rng = np.random.default_rng(21)
+    shape = (3000, 400, 900)
+    n = 12_000_000
+    cols = [np.minimum(rng.zipf(1.2, size=n) - 1, shape[0] - 1), rng.integers(0, shape[1], n),
+            rng.integers(0, shape[2], n)]
+    lin = np.unique(np.ravel_multi_index(cols, shape))
+    subs = np.column_stack(np.unravel_index(lin, shape)).astype(np.int64)
+    vals = rng.standard_normal(subs.shape[0])
+    out = []
+    for k in (1, 2):
+        x = rng.standard_normal(shape[k])
+        g, e = K.ttv_raw(subs, vals, shape, x, k), oracle.ttv_raw(subs, vals, shape, x, k)
+        out.append(g[0].tobytes() == e[0].tobytes() and g[1].tobytes() == e[1].tobytes()
+                   and tuple(g[2]) == tuple(e[2]))
+    queue.put((subs.shape[0], out))
+
+
+@pytest.mark.parametrize("env", [
+    {},                                                                     # one interval, 22-bit keys
+    {"TK_SPLIT_MIN_ROWS": "150000"},                                        # many intervals, 2-3 passes
+    {"TK_SPLIT_MIN_ROWS": "150000", "TK_SPLIT_MIN_NNZ": "1"},
+    {"TK_SPLIT_SORT": "0"},                                                 # the one-sort path
+])
+def test_general_path_split_sort_bit_exact(env):
+    """General path with the middle mode contracted on 6.9M canonical Zipf rows: the leading
+    kept mode is sorted, so rows are cut into leading-mode intervals sorted on their own with
+    32-bit keys.  Bit-exact against the oracle for k = 1 (and k = 2, the tile path), with one or
+    many intervals (fresh process per setting: the switches are read once)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_split_case, args=(q, env))
+    pr.start()
+    nrows, ok = q.get(timeout=600)
+    pr.join(timeout=60)
+    assert nrows > 6_000_000 and ok == [True, True], (env, ok)
+
+
+def _split_vs_one_sort(queue, env_off):
+    import os
+    if env_off:
+        os.environ["TK_SPLIT_SORT"] = "0"
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    t = DeviceCoo.generate((10**6, 10**5, 10**4), 50_000_000, zipf_s=1.2, normal_vals=True, seed=12345)
+    x = uniform_vector(10**5, 778)
+    u, s, v = t.ttv(x, 1)
+    queue.put((u, hashlib.sha256(s[:u].cpu().numpy().tobytes()).hexdigest(),
+               hashlib.sha256(v[:u].cpu().numpy().tobytes()).hexdigest()))
+
+
+def test_general_path_split_matches_one_sort_at_scale():
+    """Config-5 tensor shape (Zipf 1.2, 5e7 rows), middle mode: the split path and the one-sort
+    path (TK_SPLIT_SORT=0, fresh process) give the same bytes."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    res = []
+    for off in (False, True):
+        q = ctx.Queue()
+        pr = ctx.Process(target=_split_vs_one_sort, args=(q, off))
+        pr.start()
+        res.append(q.get(timeout=600))
+        pr.join(timeout=60)
+    assert res[0] == res[1]
