@@ -113,8 +113,14 @@ __global__ void __launch_bounds__(kDotThreads) dot_kernel(const double* __restri
 
 // One warp per row; 128-bit loads of the row (streamed), x through the read-only path (L1
 // resident after the first rows).  The warp butterfly fixes the combine order.
-constexpr int kMvWarps = 8;
-constexpr int kMvUnroll = 8;
+#ifndef TK_MV_UNROLL
+#define TK_MV_UNROLL 8
+#endif
+#ifndef TK_MV_WARPS
+#define TK_MV_WARPS 8
+#endif
+constexpr int kMvWarps = TK_MV_WARPS;
+constexpr int kMvUnroll = TK_MV_UNROLL;
 
 __global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __restrict__ a, long long rows,
                                                                 long long cols, const double* __restrict__ x,

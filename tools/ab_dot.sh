@@ -16,7 +16,13 @@ ts = []
 for i in range(30):
     torch.cuda.synchronize(); flush.zero_(); sink.copy_(flush.sum()); dv.dot(x, y, out)
     if i >= 5: ts.append(lib.tk_last_kernel_ms())
-print("$(basename $v .so)", round(float(np.median(ts)) * 1e3, 2), "us dot")
+ops2 = synth.host_operands(2)
+a, xv = torch.from_numpy(ops2["a"]).cuda(), torch.from_numpy(ops2["x"]).cuda(); yv = torch.empty(4096, dtype=torch.float64, device="cuda")
+tm = []
+for i in range(30):
+    torch.cuda.synchronize(); flush.zero_(); sink.copy_(flush.sum()); dv.matvec(a, xv, yv)
+    if i >= 5: tm.append(lib.tk_last_kernel_ms())
+print("$(basename $v .so)", round(float(np.median(ts)) * 1e3, 2), "us dot", round(float(np.median(tm)) * 1e3, 2), "us matvec")
 PY
 done
 cp /tmp/tk_keep.so paper_2510_01495_b200/libtk_b200.so
