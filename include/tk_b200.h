@@ -167,6 +167,42 @@ int tk_gen_coo_device(int32_t d, const int64_t* shape, int64_t nnz, double zipf_
 /* Uniform [0,1) vector from the same counter-based generator. */
 int tk_gen_uniform_device(int64_t n, uint64_t seed, double* out, void* stream);
 
+/* ---- workspace, timed forms, one-process multi-GPU ---------------------- */
+
+/* Upper bound of the device scratch a tk_ttv_f64_device call with these sizes takes from the
+ * stream-ordered pool (sorted fast path; the general sort path; the larger of the two).  The
+ * library allocates it itself; this is for callers sizing device memory. */
+int tk_ttv_workspace(int32_t d, int64_t nnz, int32_t nkeep, size_t* bytes);
+
+/* The device entry points with the call's device time: a cudaEvent pair recorded on `stream`
+ * around the whole call (elapsed_ms, host).  The reference's self-timed protocol
+ * (_ckernels.pyx:98-122, 377-388: dot_timed / matvec_timed / ttv_timed). */
+int tk_dot_f64_device_timed(const double* x, const double* y, int64_t n, double* out, void* stream,
+                            float* elapsed_ms);
+int tk_matvec_f64_device_timed(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                               void* stream, float* elapsed_ms);
+int tk_ttv_f64_device_timed(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                            const int64_t* subs, const double* vals, const double* x, int64_t nx, int32_t k,
+                            int64_t* out_subs, double* out_vals, int64_t* out_nnz, void* stream,
+                            float* elapsed_ms);
+
+/* One process driving several GPUs (the torch.distributed path runs one process per GPU
+ * instead; both shard the same way).  tk_multi_init enables peer access among
+ * `devices` and creates a stream per device.  tk_multi_ttv_f64 runs the sparse-result TTV of
+ * every shard concurrently (one host thread per shard): shard s is a contiguous row range of
+ * the canonical tensor cut at kept-key changes, resident on device shard_device[s] (SoA
+ * columns shard_cols[s][0..d), shard_vals[s], the vector shard_x[s]); its result goes to
+ * shard_out_subs[s] / shard_out_vals[s] on that device, its count to shard_out_nnz[s], and
+ * out_offsets[0..nshard] is the exclusive prefix of the counts: the rank-order concatenation is
+ * the one-GPU result, bit for bit.  The first failing shard's status is returned. */
+int tk_multi_init(int32_t ndev, const int32_t* devices);
+int tk_multi_ttv_f64(int32_t d, const int64_t* shape, int32_t k, int32_t nshard, const int32_t* shard_device,
+                     const int64_t* shard_nnz, const int64_t* const* const* shard_cols,
+                     const double* const* shard_vals, const double* const* shard_x, int64_t nx,
+                     int64_t* const* shard_out_subs, double* const* shard_out_vals, int64_t* shard_out_nnz,
+                     int64_t* out_offsets);
+int tk_multi_free(void);
+
 /* ---- timing helper ----------------------------------------------------------------------- */
 /* Device milliseconds between two points on a stream (cudaEvent pair). */
 int tk_timer_start(void* stream);

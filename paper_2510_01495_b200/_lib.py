@@ -54,6 +54,18 @@ SIGNATURES = {
     "tk_gen_coo_device": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, ctypes.c_double,
                                          ctypes.c_int32, ctypes.c_uint64, _vp, _vp, _vp]),
     "tk_gen_uniform_device": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, _vp, _vp]),
+    "tk_ttv_workspace": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                        ctypes.POINTER(ctypes.c_size_t)]),
+    "tk_dot_f64_device_timed": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, ctypes.POINTER(ctypes.c_float)]),
+    "tk_matvec_f64_device_timed": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp,
+                                                  ctypes.POINTER(ctypes.c_float)]),
+    "tk_ttv_f64_device_timed": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int64, _vp, _vp, _vp, _vp,
+                                               ctypes.c_int64, ctypes.c_int32, _vp, _vp, _c_i64p, _vp,
+                                               ctypes.POINTER(ctypes.c_float)]),
+    "tk_multi_init": (ctypes.c_int, [ctypes.c_int32, _vp]),
+    "tk_multi_ttv_f64": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp,
+                                        _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
+    "tk_multi_free": (ctypes.c_int, []),
     "tk_timer_start": (ctypes.c_int, [_vp]),
     "tk_timer_stop": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "tk_release": (ctypes.c_int, []),

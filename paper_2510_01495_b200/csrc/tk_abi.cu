@@ -12,6 +12,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tk_host.h"
@@ -505,6 +506,149 @@ int tk_ttv_dense_f64_device_peers(int32_t d, const int64_t* shape, int64_t nnz, 
     if (!outs[i]) return fail(TK_EARG, "ttv_dense_peers: null output");
   return ttv_dense_peers(d, shape, nnz, cols, vals, keep, vecs, outs, nout, key_lo, key_hi,
                          static_cast<cudaStream_t>(stream));
+}
+
+// ---- workspace, timed forms, one-process multi-GPU ----------------------------
+
+int tk_ttv_workspace(int32_t d, int64_t nnz, int32_t nkeep, size_t* bytes) {
+  if (!bytes || d < 2 || nnz < 0 || nkeep < 1) return fail(TK_EARG, "ttv_workspace: bad arguments");
+  const size_t n = (size_t)nnz;
+  const size_t tiles = n / 256 + 2;                      // smallest tile geometry
+  const size_t fast = tiles * 8 + 4096;                  // status words + counters
+  const size_t sort = n * 8 * 5 + n * 12 + (64u << 20);  // keys/w double buffers, 32-bit split keys, CUB temp
+  const size_t lsd = n * 8 * (4 + (size_t)nkeep) + (64u << 20);  // garbage-key path: permutation + sorted columns
+  *bytes = std::max(fast, std::max(sort, lsd)) + n * 8 * (size_t)d;  // + SoA transpose when subs is row-major
+  return TK_OK;
+}
+
+namespace {
+struct EventTimer {  // cudaEvent pair on `st` around a call
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  explicit EventTimer(cudaStream_t s) : st(s) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  int stop(float* ms) {
+    TK_CUDA(cudaEventRecord(b, st));
+    TK_CUDA(cudaEventSynchronize(b));
+    TK_CUDA(cudaEventElapsedTime(ms, a, b));
+    return TK_OK;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+}  // namespace
+
+int tk_dot_f64_device_timed(const double* x, const double* y, int64_t n, double* out, void* stream,
+                            float* elapsed_ms) {
+  if (!elapsed_ms) return fail(TK_EARG, "dot_timed: null elapsed_ms");
+  EventTimer t(static_cast<cudaStream_t>(stream));
+  if (int rc = tk_dot_f64_device(x, y, n, out, stream)) return rc;
+  return t.stop(elapsed_ms);
+}
+
+int tk_matvec_f64_device_timed(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                               void* stream, float* elapsed_ms) {
+  if (!elapsed_ms) return fail(TK_EARG, "matvec_timed: null elapsed_ms");
+  EventTimer t(static_cast<cudaStream_t>(stream));
+  if (int rc = tk_matvec_f64_device(a, rows, cols, x, y, stream)) return rc;
+  return t.stop(elapsed_ms);
+}
+
+int tk_ttv_f64_device_timed(int32_t d, const int64_t* shape, int64_t nnz, const int64_t* const* cols,
+                            const int64_t* subs, const double* vals, const double* x, int64_t nx, int32_t k,
+                            int64_t* out_subs, double* out_vals, int64_t* out_nnz, void* stream,
+                            float* elapsed_ms) {
+  if (!elapsed_ms) return fail(TK_EARG, "ttv_timed: null elapsed_ms");
+  EventTimer t(static_cast<cudaStream_t>(stream));
+  if (int rc = tk_ttv_f64_device(d, shape, nnz, cols, subs, vals, x, nx, k, out_subs, out_vals, out_nnz, stream))
+    return rc;
+  return t.stop(elapsed_ms);
+}
+
+namespace {
+std::mutex g_multi_mu;
+std::vector<int> g_multi_dev;
+std::vector<cudaStream_t> g_multi_st;
+}  // namespace
+
+int tk_multi_init(int32_t ndev, const int32_t* devices) {
+  if (ndev < 1 || !devices) return fail(TK_EARG, "multi_init: bad arguments");
+  std::lock_guard<std::mutex> lk(g_multi_mu);
+  int prev = 0;
+  TK_CUDA(cudaGetDevice(&prev));
+  for (cudaStream_t s : g_multi_st) cudaStreamDestroy(s);
+  g_multi_dev.assign(devices, devices + ndev);
+  g_multi_st.assign(ndev, nullptr);
+  for (int i = 0; i < ndev; ++i) {
+    TK_CUDA(cudaSetDevice(devices[i]));
+    TK_CUDA(cudaStreamCreateWithFlags(&g_multi_st[i], cudaStreamNonBlocking));
+    for (int j = 0; j < ndev; ++j) {
+      if (devices[j] == devices[i]) continue;
+      int can = 0;
+      TK_CUDA(cudaDeviceCanAccessPeer(&can, devices[i], devices[j]));
+      if (can) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+    }
+  }
+  TK_CUDA(cudaSetDevice(prev));
+  return TK_OK;
+}
+
+int tk_multi_ttv_f64(int32_t d, const int64_t* shape, int32_t k, int32_t nshard, const int32_t* shard_device,
+                     const int64_t* shard_nnz, const int64_t* const* const* shard_cols,
+                     const double* const* shard_vals, const double* const* shard_x, int64_t nx,
+                     int64_t* const* shard_out_subs, double* const* shard_out_vals, int64_t* shard_out_nnz,
+                     int64_t* out_offsets) {
+  if (int rc = check_ttv_args(d, shape, k, nx)) return rc;
+  if (nshard < 1 || !shard_device || !shard_nnz || !shard_cols || !shard_vals || !shard_x || !shard_out_subs ||
+      !shard_out_vals || !shard_out_nnz || !out_offsets)
+    return fail(TK_EARG, "multi_ttv: bad arguments");
+  std::vector<cudaStream_t> st(nshard);
+  {
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    for (int s = 0; s < nshard; ++s) {
+      size_t i = 0;
+      while (i < g_multi_dev.size() && g_multi_dev[i] != shard_device[s]) ++i;
+      if (i == g_multi_dev.size()) return fail(TK_EARG, "multi_ttv: shard device not in tk_multi_init's list");
+      st[s] = g_multi_st[i];
+    }
+  }
+  std::vector<int> rcs(nshard, TK_OK);
+  std::vector<std::string> errs(nshard);
+  std::vector<std::thread> th;
+  for (int s = 0; s < nshard; ++s)
+    th.emplace_back([&, s] {
+      if (cudaSetDevice(shard_device[s]) != cudaSuccess) {
+        rcs[s] = TK_ECUDA;
+        errs[s] = "cudaSetDevice failed";
+        return;
+      }
+      rcs[s] = tk_ttv_f64_device(d, shape, shard_nnz[s], shard_cols[s], nullptr, shard_vals[s], shard_x[s], nx, k,
+                                 shard_out_subs[s], shard_out_vals[s], &shard_out_nnz[s], st[s]);
+      if (rcs[s]) errs[s] = tk_last_error();
+    });
+  for (auto& t : th) t.join();
+  for (int s = 0; s < nshard; ++s)
+    if (rcs[s]) return fail(rcs[s], errs[s]);  // the error message is thread-local: carry it over
+  out_offsets[0] = 0;
+  for (int s = 0; s < nshard; ++s) out_offsets[s + 1] = out_offsets[s] + shard_out_nnz[s];
+  return TK_OK;
+}
+
+int tk_multi_free(void) {
+  std::lock_guard<std::mutex> lk(g_multi_mu);
+  for (cudaStream_t s : g_multi_st) cudaStreamDestroy(s);
+  g_multi_st.clear();
+  g_multi_dev.clear();
+  return TK_OK;
 }
 
 int tk_ipc_alloc(int64_t bytes, void** dev_ptr) {

@@ -21,7 +21,9 @@ def declared_symbols():
 def test_header_declares_the_expected_surface():
     syms = declared_symbols()
     for s in ("tk_ttv_f64_device", "tk_ttv_f64_host", "tk_dot_f64_host", "tk_matvec_f64_host",
-              "tk_ttv_dense_f64_device", "tk_group_sum_f64_host", "tk_last_error"):
+              "tk_ttv_dense_f64_device", "tk_group_sum_f64_host", "tk_last_error", "tk_ttv_workspace",
+              "tk_ttv_f64_device_timed", "tk_dot_f64_device_timed", "tk_matvec_f64_device_timed",
+              "tk_multi_init", "tk_multi_ttv_f64", "tk_multi_free", "tk_ttv_dense_f64_device_peers"):
         assert s in syms
 
 
@@ -77,3 +79,14 @@ def test_structural_guards_raise_before_any_device_work():
         kernels.dot(np.ones(3), np.ones(4))
     with pytest.raises(errors.DimensionError):
         kernels.matvec(np.ones((2, 3)), np.ones(2))
+
+
+def test_ttv_workspace_is_host_arithmetic():
+    """tk_ttv_workspace needs no GPU: an upper bound that grows with nnz and rejects bad sizes."""
+    import ctypes
+    lib = _lib.load()
+    b1, b2 = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert lib.tk_ttv_workspace(3, 1_000_000, 2, ctypes.byref(b1)) == 0
+    assert lib.tk_ttv_workspace(3, 4 * 10**8, 2, ctypes.byref(b2)) == 0
+    assert b2.value > b1.value >= 1_000_000 * 8 * 3
+    assert lib.tk_ttv_workspace(1, 10, 0, ctypes.byref(b1)) != 0

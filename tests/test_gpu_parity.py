@@ -681,3 +681,55 @@ def test_general_path_split_matches_one_sort_at_scale():
         res.append(q.get(timeout=600))
         pr.join(timeout=60)
     assert res[0] == res[1]
+
+
+def test_c_abi_timed_and_one_process_multi_device(oracle):
+    """The timed device entry points (event pair around the call) and tk_multi_ttv_f64: three
+    key-aligned shards, all on device 0 here (one host thread per shard), concatenate to the
+    one-call result bit for bit; offsets are the exclusive prefix of the shard counts."""
+    import ctypes
+    import torch
+    from paper_2510_01495_b200 import _lib, multi
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    lib = _lib.load()
+    shape = (2000, 300, 400)
+    t = DeviceCoo.generate(shape, 3_000_000, zipf_s=1.1, normal_vals=True, seed=5)
+    x = uniform_vector(shape[2], 9)
+    u0, s0, v0 = t.ttv(x, 2)
+    ms = ctypes.c_float(-1.0)
+    os_ = torch.empty((t.nnz, 2), dtype=torch.int64, device="cuda")
+    ov = torch.empty(t.nnz, dtype=torch.float64, device="cuda")
+    u = ctypes.c_int64(0)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.tk_ttv_f64_device_timed(3, _lib.i64_array(shape), t.nnz,
+                                           _lib.ptr_array([c.data_ptr() for c in t.cols]), None, t.vals.data_ptr(),
+                                           x.data_ptr(), shape[2], 2, os_.data_ptr(), ov.data_ptr(), ctypes.byref(u),
+                                           st, ctypes.byref(ms)))
+    assert u.value == u0 and ms.value > 0
+    assert torch.equal(os_[:u0], s0[:u0]) and torch.equal(ov[:u0], v0[:u0])
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.check(lib.tk_dot_f64_device_timed(t.vals.data_ptr(), t.vals.data_ptr(), t.nnz, out.data_ptr(), st,
+                                           ctypes.byref(ms)))
+    assert ms.value > 0
+    # one process, three shards on device 0
+    key = multi.kept_prefix_key(t.cols, 2, shape)
+    bounds = multi.shard_bounds(key, 3)
+    shards = [t.slice(bounds[i], bounds[i + 1]) for i in range(3)]
+    outs = [(torch.empty((max(sh.nnz, 1), 2), dtype=torch.int64, device="cuda"),
+             torch.empty(max(sh.nnz, 1), dtype=torch.float64, device="cuda")) for sh in shards]
+    dev = (ctypes.c_int32 * 3)(0, 0, 0)
+    _lib.check(lib.tk_multi_init(1, (ctypes.c_int32 * 1)(0)))
+    col_arrays = [_lib.ptr_array([c.data_ptr() for c in sh.cols]) for sh in shards]
+    cols_pp = (ctypes.c_void_p * 3)(*[ctypes.cast(a, ctypes.c_void_p).value for a in col_arrays])
+    nnz = (ctypes.c_int64 * 3)(*[sh.nnz for sh in shards])
+    counts, offs = (ctypes.c_int64 * 3)(), (ctypes.c_int64 * 4)()
+    _lib.check(lib.tk_multi_ttv_f64(3, _lib.i64_array(shape), 2, 3, dev, nnz, cols_pp,
+                                    _lib.ptr_array([sh.vals.data_ptr() for sh in shards]),
+                                    _lib.ptr_array([x.data_ptr()] * 3), shape[2],
+                                    _lib.ptr_array([o[0].data_ptr() for o in outs]),
+                                    _lib.ptr_array([o[1].data_ptr() for o in outs]), counts, offs))
+    _lib.check(lib.tk_multi_free())
+    assert list(offs) == [0, counts[0], counts[0] + counts[1], u0]
+    cat_s = torch.cat([outs[i][0][:counts[i]] for i in range(3)])
+    cat_v = torch.cat([outs[i][1][:counts[i]] for i in range(3)])
+    assert torch.equal(cat_s, s0[:u0]) and torch.equal(cat_v, v0[:u0])
