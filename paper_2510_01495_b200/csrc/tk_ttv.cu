@@ -86,6 +86,8 @@ constexpr int kMaxParts = 64;
 struct PartTable {
   long long lo[kMaxParts + 1];  // leading-mode value where each part starts
   int nparts;
+  unsigned long long in_b;      // bit j: part j's (key, w) go to the second buffers (odd digit-pass
+                                // count, so the sorted w ends in the first one: no copy in widen)
 };
 
 // w = vals * x[subk] and the 32-bit part-local key (lead - lo[part]) * R + rest, where rest is the
@@ -93,7 +95,7 @@ struct PartTable {
 __global__ void prep_key32_kernel(long long n, int nk, KeepCols kc, const long long* __restrict__ subk,
                                   const double* __restrict__ vals, const double* __restrict__ x, long long nx,
                                   PartTable pt, unsigned int* __restrict__ key, double* __restrict__ w,
-                                  Counters* ctr) {
+                                  unsigned int* __restrict__ key_b, double* __restrict__ w_b, Counters* ctr) {
   unsigned int flags = 0;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
     const long long idx = subk[r];
@@ -114,8 +116,9 @@ __global__ void prep_key32_kernel(long long n, int nk, KeepCols kc, const long l
       rest = rest * kc.dims[c] + v;
       R *= kc.dims[c];
     }
-    key[r] = (unsigned int)((lead - pt.lo[lo]) * R + rest);
-    w[r] = wr;
+    const bool b = (pt.in_b >> lo) & 1ull;
+    (b ? key_b : key)[r] = (unsigned int)((lead - pt.lo[lo]) * R + rest);
+    (b ? w_b : w)[r] = wr;
   }
   if (flags) atomicOr(&ctr->flags, flags);
 }
@@ -832,6 +835,7 @@ int ttv_general_split(long long nnz, int nk, const KeepCols& kc, const std::vect
     int bits = 1;
     while (bits < 32 && (maxkey >> bits)) ++bits;
     pbits.push_back(bits);
+    if (((bits + 7) / 8) & 1) pt.in_b |= 1ull << (pt.nparts - 1);  // CUB onesweep: 8-bit digits
     a = b;
   }
   pt.lo[pt.nparts] = n0;
@@ -843,7 +847,8 @@ int ttv_general_split(long long nnz, int nk, const KeepCols& kc, const std::vect
   if (int rc = wb.alloc(nnz * 8, st)) return rc;
   if (int rc = keys.alloc(nnz * 8, st)) return rc;
   prep_key32_kernel<<<g, 256, 0, st>>>(nnz, nk, kc, reinterpret_cast<const long long*>(cols[k]), vals, x, nx, pt,
-                                       k32a.as<unsigned int>(), wa.as<double>(), dctr);
+                                       k32a.as<unsigned int>(), wa.as<double>(), k32b.as<unsigned int>(),
+                                       wb.as<double>(), dctr);
   count_launch();
   TK_CUDA(cudaGetLastError());
   TK_CUDA(cudaMemcpyAsync(hc, dctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -863,8 +868,11 @@ int ttv_general_split(long long nnz, int nk, const KeepCols& kc, const std::vect
   for (int j = 0; j < pt.nparts; ++j) {
     const long long r0 = off[pt.lo[j]], rows = off[pt.lo[j + 1]] - r0;
     if (rows == 0) continue;
-    cub::DoubleBuffer<unsigned int> kb(k32a.as<unsigned int>() + r0, k32b.as<unsigned int>() + r0);
-    cub::DoubleBuffer<double> vb(wa.as<double>() + r0, wb.as<double>() + r0);
+    const bool in_b = (pt.in_b >> j) & 1ull;
+    unsigned int *ka = k32a.as<unsigned int>() + r0, *kbb = k32b.as<unsigned int>() + r0;
+    double *va = wa.as<double>() + r0, *vbb = wb.as<double>() + r0;
+    cub::DoubleBuffer<unsigned int> kb(in_b ? kbb : ka, in_b ? ka : kbb);
+    cub::DoubleBuffer<double> vb(in_b ? vbb : va, in_b ? va : vbb);
     size_t tbj = tb;
     TK_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbj, kb, vb, (int)rows, 0, pbits[j], st));
     widen_part_kernel<<<grid_for(rows), 256, 0, st>>>(rows, kb.Current(), vb.Current(), pt.lo[j] * R,
