@@ -30,7 +30,13 @@ namespace tk {
 
 namespace {
 
-constexpr int kMtSpan = 1024;     // rows per warp span (carry unit)
+#ifndef TK_MT_SPAN
+#define TK_MT_SPAN 1024
+#endif
+#ifndef TK_MT_BATCH
+#define TK_MT_BATCH 4  // gathers issued per batch, in groups of rows (8: R=16 3.77 ms; 4: 3.28 ms; 2, 1: slower)
+#endif
+constexpr int kMtSpan = TK_MT_SPAN;  // rows per warp span (carry unit)
 constexpr int kMtThreads = 256;   // 8 warps per CTA
 constexpr int kMtWarps = kMtThreads / 32;
 
@@ -61,7 +67,7 @@ template <int D, int RP, int RPL, bool PERM>
 __global__ void __launch_bounds__(kMtThreads) mttkrp_kernel(MtParams p, long long nspans) {
   constexpr int DM = D > 0 ? D : kMaxOrder;
   constexpr int G = 32 / RP;
-  constexpr int B = 8 / RPL;  // groups per gather batch
+  constexpr int B = TK_MT_BATCH / RPL > 0 ? TK_MT_BATCH / RPL : 1;  // groups per gather batch
   static_assert(RP == 32 || RPL == 1, "several columns per lane only with full-warp rows");
   __shared__ long long s_off[kMtWarps][DM][32];  // factor-row offsets idx*R (column 0 unused)
   __shared__ long long s_key[kMtWarps][32];
