@@ -67,7 +67,9 @@ template <int D, int RP, int RPL, bool PERM>
 __global__ void __launch_bounds__(kMtThreads) mttkrp_kernel(MtParams p, long long nspans) {
   constexpr int DM = D > 0 ? D : kMaxOrder;
   constexpr int G = 32 / RP;
-  constexpr int B = TK_MT_BATCH / RPL > 0 ? TK_MT_BATCH / RPL : 1;  // groups per gather batch
+  // groups per gather batch (narrow rows, RP <= 4: twice as many -- a group is only 4 gathers wide)
+  constexpr int BT = RP <= 4 ? 2 * TK_MT_BATCH : TK_MT_BATCH;
+  constexpr int B = BT / RPL > 0 ? BT / RPL : 1;
   static_assert(RP == 32 || RPL == 1, "several columns per lane only with full-warp rows");
   __shared__ long long s_off[kMtWarps][DM][32];  // factor-row offsets idx*R (column 0 unused)
   __shared__ long long s_key[kMtWarps][32];
