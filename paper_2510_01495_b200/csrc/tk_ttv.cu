@@ -291,7 +291,7 @@ __global__ void bcast_range_kernel(const double* __restrict__ src, PeerOuts o, l
 }
 
 #ifndef TK_DENSE_SPAN
-#define TK_DENSE_SPAN 2048
+#define TK_DENSE_SPAN 3072  // rows per warp span (config 4: 2048 0.868 ms, 3072 0.832, 3584 0.830, 4096 0.884)
 #endif
 #ifndef TK_DENSE_U
 #define TK_DENSE_U 1
