@@ -37,7 +37,10 @@ namespace {
 #define TK_MT_BATCH 4  // gathers issued per batch, in groups of rows (8: R=16 3.77 ms; 4: 3.28 ms; 2, 1: slower)
 #endif
 constexpr int kMtSpan = TK_MT_SPAN;  // rows per warp span (carry unit)
-constexpr int kMtThreads = 256;   // 8 warps per CTA
+#ifndef TK_MT_THREADS
+#define TK_MT_THREADS 256
+#endif
+constexpr int kMtThreads = TK_MT_THREADS;  // warps per CTA x 32
 constexpr int kMtWarps = kMtThreads / 32;
 
 struct MtParams {
