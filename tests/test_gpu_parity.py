@@ -634,6 +634,42 @@ def _split_case(queue, env):
     queue.put((subs.shape[0], out))
 
 
+def _split_case4(queue, env):
+    import os
+    os.environ.update(env)
+    from oracle import oracle
+    from paper_2510_01495_b200 import backend
+    K = backend.kernels()
+    rng = np.random.default_rng(33)
+    shape = (2000, 60, 50, 40)
+    n = 9_000_000
+    cols = [np.minimum(rng.zipf(1.1, size=n) - 1, shape[0] - 1)] + [rng.integers(0, m, n) for m in shape[1:]]
+    lin = np.unique(np.ravel_multi_index(cols, shape))
+    subs = np.column_stack(np.unravel_index(lin, shape)).astype(np.int64)
+    vals = rng.standard_normal(subs.shape[0])
+    out = []
+    for k in (1, 2):
+        x = rng.standard_normal(shape[k])
+        g, e = K.ttv_raw(subs, vals, shape, x, k), oracle.ttv_raw(subs, vals, shape, x, k)
+        out.append(g[0].tobytes() == e[0].tobytes() and g[1].tobytes() == e[1].tobytes())
+    queue.put((subs.shape[0], out))
+
+
+@pytest.mark.parametrize("env", [{"TK_SPLIT_MIN_NNZ": "1"},
+                                 {"TK_SPLIT_MIN_NNZ": "1", "TK_SPLIT_MIN_ROWS": "100000"}])
+def test_general_path_split_sort_order4(env):
+    """Order-4 tensor, contracted mode 1 or 2 (R = product of two kept dims): the split path's
+    part-local keys over three kept modes, one or many intervals; bit-exact against the oracle."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_split_case4, args=(q, env))
+    pr.start()
+    nrows, ok = q.get(timeout=600)
+    pr.join(timeout=60)
+    assert nrows > 3_000_000 and ok == [True, True], (env, nrows, ok)
+
+
 @pytest.mark.parametrize("env", [
     {},                                                                     # one interval, 22-bit keys
     {"TK_SPLIT_MIN_ROWS": "150000"},                                        # many intervals, 2-3 passes
