@@ -64,19 +64,31 @@ __global__ void prep_linkey_kernel2(long long n, int nk, KeepCols kc, const long
 // kFlagUnsorted if col0 decreases and kFlagKeptOob if it leaves [0, n0): the split is then off.
 __global__ void lead_offsets_kernel(long long n, const long long* __restrict__ col0, long long n0,
                                     long long* __restrict__ off, Counters* ctr) {
+  constexpr int U = 4;  // rows per thread per round, every load of the round in flight at once
   unsigned int flags = 0;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= n; r += (long long)gridDim.x * blockDim.x) {
-    const long long prev = r == 0 ? -1 : col0[r - 1];
-    const long long cur = r == n ? n0 : col0[r];
-    if (r < n && (cur < 0 || cur >= n0)) {
-      flags |= kFlagKeptOob;
-      continue;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long r0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; r0 <= n; r0 += U * stride) {
+    long long prev[U], cur[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long r = r0 + u * stride;
+      prev[u] = (r == 0 || r > n) ? -1 : __ldg(col0 + r - 1);
+      cur[u] = r < n ? __ldg(col0 + r) : n0;
     }
-    if (cur < prev) {
-      flags |= kFlagUnsorted;
-      continue;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long r = r0 + u * stride;
+      if (r > n) break;
+      if (r < n && (cur[u] < 0 || cur[u] >= n0)) {
+        flags |= kFlagKeptOob;
+        continue;
+      }
+      if (cur[u] < prev[u]) {
+        flags |= kFlagUnsorted;
+        continue;
+      }
+      for (long long v = prev[u] + 1; v <= cur[u] && v <= n0; ++v) off[v] = r;
     }
-    for (long long v = prev + 1; v <= cur && v <= n0; ++v) off[v] = r;
   }
   if (flags) atomicOr(&ctr->flags, flags);
 }
