@@ -76,6 +76,21 @@ def gather_counts(u: int, device) -> list:
     return [int(v.item()) for v in out]
 
 
+def gather_counts_async(u: int, device):
+    """Start the all-gather of per-rank output counts without waiting for it (the next step's
+    TTV kernel runs while it completes); finish with ``wait_counts``."""
+    world = dist.get_world_size()
+    t = torch.tensor([u], dtype=torch.int64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    return dist.all_gather(out, t, async_op=True), out
+
+
+def wait_counts(handle) -> list:
+    work, out = handle
+    work.wait()
+    return [int(v.item()) for v in out]
+
+
 def global_offsets(counts) -> list:
     off = [0]
     for c in counts:
