@@ -493,8 +493,14 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       long long* o = p.out_subs + g * p.out_nk;
       for (int q = p.out_nk - 1; q >= 0; --q) {
         const long long dm = p.dims[q];
-        o[q] = lin % dm;
-        lin /= dm;
+        if (p.lin_fast) {  // multiply + fix-up instead of a 64-bit division
+          long long rem;
+          lin = divmod_fast(lin, dm, p.inv_dims[q], &rem);
+          o[q] = rem;
+        } else {
+          o[q] = lin % dm;
+          lin /= dm;
+        }
       }
     } else {
       if constexpr (NK == 2) {

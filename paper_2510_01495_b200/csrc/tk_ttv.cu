@@ -784,6 +784,17 @@ int lin_bits(const std::vector<long long>& dims) {
   return std::max(bits, 1);
 }
 
+// Kept dims for decoding linear keys; the multiply-based decode when every key is < 2^52.
+void set_lin_dims(SegParams& p, int nk, const std::vector<long long>& dims) {
+  double prod = 1.0;
+  for (int c = 0; c < nk; ++c) {
+    p.dims[c] = dims[c];
+    p.inv_dims[c] = 1.0 / (double)dims[c];
+    prod *= (double)dims[c];
+  }
+  p.lin_fast = prod < 4503599627370496.0;  // 2^52
+}
+
 constexpr int kDeclined = -1;  // the split path does not apply: take the one-sort path
 
 long long kSplitMinNnz() {  // TK_SPLIT_MIN_NNZ: smallest stream the split path takes (tests lower it)
@@ -898,7 +909,7 @@ int ttv_general_split(long long nnz, int nk, const KeepCols& kc, const std::vect
   p.key[0] = keys.as<long long>();
   p.a = wa.as<double>();
   p.out_nk = nk;
-  for (int c = 0; c < nk; ++c) p.dims[c] = dims[c];
+  set_lin_dims(p, nk, dims);
   p.out_subs = reinterpret_cast<long long*>(out_subs);
   p.out_vals = out_vals;
   p.bulk_ok = aligned16(p.key[0]) && aligned16(p.a);
@@ -968,7 +979,7 @@ int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const
     p.key[0] = kb.Current();
     p.a = vb.Current();
     p.out_nk = nk;
-    for (int c = 0; c < nk; ++c) p.dims[c] = dims[c];
+    set_lin_dims(p, nk, dims);
     p.out_subs = reinterpret_cast<long long*>(out_subs);
     p.out_vals = out_vals;
     p.bulk_ok = aligned16(p.key[0]) && aligned16(p.a);

@@ -34,6 +34,8 @@ struct SegParams {
   long long nx;
   int out_nk;                        // output columns (= d - 1)
   long long dims[kMaxKeep];          // kSrcLinKey: kept dims for decoding
+  double inv_dims[kMaxKeep];         // kSrcLinKey: 1.0 / dims (decoding by multiply + fix-up when
+  int lin_fast;                      //   every key is < 2^52, so doubles hold it exactly)
   long long* out_subs;               // row-major (groups, out_nk)
   double* out_vals;
   unsigned long long* status;        // look-back words, one per tile (zeroed)
@@ -60,15 +62,37 @@ __device__ __forceinline__ int seg_nk(const SegParams& p) {
 }
 
 // lexicographic compare of stream row a (in smem) with a key vector b: -1, 0, 1
+// lin / dm and lin % dm for lin < 2^52 without a 64-bit division: the double estimate of the
+// quotient is off by at most one, and the remainder fixes it.
+__device__ __forceinline__ long long divmod_fast(long long lin, long long dm, double inv, long long* rem) {
+  long long q = (long long)((double)lin * inv);
+  long long r = lin - q * dm;
+  if (r < 0) {
+    --q;
+    r += dm;
+  } else if (r >= dm) {
+    ++q;
+    r -= dm;
+  }
+  *rem = r;
+  return q;
+}
+
 template <int SRC>
 __device__ __forceinline__ void seg_emit(const SegParams& p, long long g, const long long* keyvals, double acc) {
   long long* o = p.out_subs + g * p.out_nk;
   if constexpr (SRC == kSrcLinKey) {
     long long lin = keyvals[0];
     for (int c = p.out_nk - 1; c >= 0; --c) {
-      long long dm = p.dims[c];
-      o[c] = lin % dm;
-      lin /= dm;
+      const long long dm = p.dims[c];
+      if (p.lin_fast) {
+        long long rem;
+        lin = divmod_fast(lin, dm, p.inv_dims[c], &rem);
+        o[c] = rem;
+      } else {
+        o[c] = lin % dm;
+        lin /= dm;
+      }
     }
   } else {
     for (int c = 0; c < p.out_nk; ++c) o[c] = keyvals[c];
