@@ -746,14 +746,14 @@ int tk_mttkrp_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64
     cp[m] = b_soa.as<int64_t>() + (size_t)m * pitch;
     if (m == n) continue;
     double* dst = b_fac.as<double>() + off;
-    if (shape[m] * rank)
+    if (shape[m] > 0 && rank > 0)
       TK_CUDA(cudaMemcpyAsync(dst, factors[m], (size_t)shape[m] * rank * 8, cudaMemcpyHostToDevice, st));
     fp[m] = dst;
     off += (size_t)pitch_of(shape[m] * rank);
   }
   if (int rc = mttkrp_device(d, shape, nnz, cp.data(), b_vals.as<double>(), n, rank, fp.data(), b_out.as<double>(), st))
     return rc;
-  if (shape[n] * rank)
+  if (shape[n] > 0 && rank > 0)
     TK_CUDA(cudaMemcpyAsync(out, b_out.get(), (size_t)shape[n] * rank * 8, cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
   return TK_OK;
