@@ -555,6 +555,7 @@ def run_ours(args):
                        "l2": "inputs (12.8 GB) larger than L2; no flush", "gen_seconds": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "frac_vs_nominal_8000": achieved / 8000.0,
                          "kernel": "ttv_tile_kernel<Raw,2,768,32>", "kernel_ms": kern_ms,
                          "alg_bytes_per_launch": alg_bytes},
             "clocks": clocks.summary(),
