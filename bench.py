@@ -3,23 +3,33 @@
 Headline workload: BASELINE config 5 -- skewed 3-way COO tensor 1e6 x 1e5 x 1e4 with
 4e8 distinct Zipf(1.2) coordinates, N(0,1) values, contracted in mode 2 (0-based) with a
 uniform length-1e4 vector; sparse 1e6 x 1e5 result.  A "step" is one full TTV over the
-tensor (all ranks' shards), through the C ABI (tk_ttv_f64_device), including the host
+tensor (all ranks' shards) through the C ABI (tk_ttv_f64_device), including the host
 read-back of the result count.  Inputs (12.8 GB) exceed the 126 MB L2, so no flush is
 needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 5] [--nnz NNZ] [--no-secondary] [--no-e2e]
+                  [--nnz NNZ] [--no-secondary] [--no-e2e] [--no-cpu]
 
-N > 1: launched by torchrun, one process per GPU, NCCL; nnz sharded at key changes
-(multi.shard_bounds), the merge is an all-gather of per-rank counts inside the timed
-region; time = max over ranks of device time (CUDA events).
+--gpus N > 1: one process per GPU over NCCL.  Under torchrun (WORLD_SIZE set) WORLD_SIZE must
+equal N; launched directly, bench.py starts torch.distributed.run itself with N ranks, and fails
+if fewer than N GPUs are visible (TK_BENCH_ONE_GPU=1 + TK_BENCH_BACKEND=gloo: path check with
+every rank on device 0, never a measurement).  nnz are sharded at key changes
+(multi.shard_bounds); the merge is an all-gather of per-rank counts inside the timed region; time
+= max over ranks of device time (CUDA events).
+
+--impl reference: the reference's own compiled TTV (oracle/_ref, built from /root/reference's
+.pyx) on every host thread over the SAME config-5 tensor, built on the host by the generator's
+host twin (oracle/tk_gen_host.cpp, byte-identical to the device generator); the product package
+is never imported on that path.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,6 +42,8 @@ sys.path.insert(0, REPO)
 
 CFG5 = {"shape": (10**6, 10**5, 10**4), "nnz": 4 * 10**8, "k": 2, "zipf_s": 1.2, "seed": 12345, "xseed": 777}
 CFG4 = {"shape": (20000,) * 4, "nnz": 10**8, "keep": 0, "seed": 4444}
+METRIC = "sparse TTV throughput (config 5, skewed Zipf 4e8 nnz)"
+WORKLOAD = "cfg5_ttv_zipf_1e6x1e5x1e4_nnz4e8_mode2"
 
 
 def peaks():
@@ -48,7 +60,7 @@ class ClockSampler:
 
     Reads the same NVML counters nvidia-smi prints (clocks.sm, clocks.max.sm,
     clocks_event_reasons.*) from a background thread every ~2 ms, so even a timed region
-    of a few tens of milliseconds gets samples.  Falls back to an nvidia-smi subprocess.
+    of a few tens of milliseconds gets samples.
     """
 
     def __init__(self, index: int, period_s: float = 0.002):
@@ -115,6 +127,27 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "source": "nvml (nvidia-smi counters), 2 ms period"}
 
 
+# ---- process topology --------------------------------------------------------------------------
+
+def launch_ranks(args) -> int:
+    """``--gpus N`` without torchrun: start N ranks with torch.distributed.run (one process per
+    GPU, NCCL).  Fails if fewer than N GPUs are visible, unless the one-GPU path check is asked
+    for (TK_BENCH_ONE_GPU=1)."""
+    import torch
+    n = args.gpus
+    have = torch.cuda.device_count()
+    if have < n and os.environ.get("TK_BENCH_ONE_GPU") != "1":
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have} "
+              "(TK_BENCH_ONE_GPU=1 TK_BENCH_BACKEND=gloo runs a path check on one GPU)", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -125,6 +158,8 @@ def dist_setup(args):
         # TK_BENCH_ONE_GPU=1 + TK_BENCH_BACKEND=gloo: path check only -- every rank on device 0,
         # collectives on the host (no kernel waits on another rank); never a measurement
         dev = 0 if os.environ.get("TK_BENCH_ONE_GPU") == "1" else local
+        if dev >= torch.cuda.device_count():
+            raise SystemExit(f"rank {rank}: device {dev} not visible ({torch.cuda.device_count()} GPUs)")
         torch.cuda.set_device(dev)
         backend = os.environ.get("TK_BENCH_BACKEND", "nccl")
         if backend == "nccl":
@@ -167,125 +202,127 @@ def cpu_info():
     return os.cpu_count(), aff
 
 
-# ---- CPU legs (oracle = checker / baseline only) ----------------------------------------------
-
-def cpu_reference_ttv(subs, vals, shape, x, k, repeats=1):
-    """Time the reference's own compiled kernel (oracle/_ref) or, if absent, the C port."""
-    from oracle import oracle
-    ck = oracle.reference_module()
-    best = None
-    for _ in range(repeats):
-        if ck is not None:
-            (_, v, _), el = ck.ttv_timed(subs, vals, tuple(shape), x, k)
-            kind = "reference"
-        else:
-            t0 = time.perf_counter()
-            _, v, _ = oracle.ttv_raw(subs, vals, shape, x, k)
-            el = time.perf_counter() - t0
-            kind = "port"
-        best = el if best is None else min(best, el)
-    return best, kind, len(v)
+def digest(subs, vals) -> dict:
+    """sha256 of a TTV result's row-major subs and vals bytes (oracle.result_digest's definition)."""
+    return {"u": int(len(vals)), "subs_sha256": hashlib.sha256(np.ascontiguousarray(subs).data).hexdigest(),
+            "vals_sha256": hashlib.sha256(np.ascontiguousarray(vals).data).hexdigest()}
 
 
-def cpu_reference_ttv_threads(subs, vals, shape, x, k, threads):
-    """The reference's compiled kernel on every host thread: the sample is cut into `threads`
-    contiguous shards at kept-key changes (multi.shard_bounds_np, so no group spans two shards and
-    the concatenation is the one-call result) and each shard runs `ttv_raw(..., release_gil=True)`
-    (the reference's own GIL-free call, _ckernels.pyx:370-374) on its own Python thread.  Wall
-    time of the whole batch.  Falls back to the C port (ctypes also drops the GIL)."""
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle import oracle
-    from paper_2510_01495_b200 import multi
-    ck = oracle.reference_module()
-    kind = "reference" if ck is not None else "port"
-    nk = len(shape) - 1
-    key = subs[:, 0].copy()
-    for m in range(1, nk):
-        key = key * int(shape[m]) + subs[:, m]
-    bounds = multi.shard_bounds_np(key, threads)
-    del key
-
-    def run(i):
-        lo, hi = bounds[i], bounds[i + 1]
-        if hi <= lo:
-            return 0
-        if ck is not None:
-            _, v, _ = ck.ttv_raw(subs[lo:hi], vals[lo:hi], tuple(shape), x, k, True)
-        else:
-            _, v, _ = oracle.ttv_raw(subs[lo:hi], vals[lo:hi], shape, x, k)
-        return len(v)
-    with ThreadPoolExecutor(threads) as ex:
-        t0 = time.perf_counter()
-        u = sum(ex.map(run, range(threads)))
-        el = time.perf_counter() - t0
-    return el, kind, u
-
-
-def sample_prefix(t, rows: int):
-    """Host copy of a prefix of the device tensor, cut at a kept-key change."""
-    import torch
-    from paper_2510_01495_b200 import multi
-    rows = min(rows, t.nnz)
-    key = multi.kept_prefix_key(t.cols, t.ndim - 1, t.shape)
-    if rows < t.nnz:
-        rows = int(torch.searchsorted(key, key[rows - 1:rows], right=True).item())
-    subs = torch.stack([c[:rows] for c in t.cols], dim=1).cpu().numpy()
-    vals = t.vals[:rows].cpu().numpy()
-    return np.ascontiguousarray(subs), vals
-
-
-# ---- reference arm ---------------------------------------------------------------------------
+# ---- reference arm -----------------------------------------------------------------------------
 
 def run_reference(args):
+    """The reference's compiled ttv_raw (oracle/_ref) on the full config-5 tensor, on every host
+    thread: the tensor is cut into one key-aligned shard per thread (oracle.shard_bounds; the
+    concatenation is the one-call result) and each shard runs ``ttv_raw(..., release_gil=True)``
+    on its own thread.  Operands come from the host twin of the device generator, so this is the
+    same tensor our arm generates on the GPU (tests/test_gen_twin.py).  Only oracle/ is used."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import torch
-    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
-    torch.cuda.set_device(0)
-    cfg = dict(CFG5)
+    from oracle import oracle  # CPU reference arm: oracle/_ref + the host twin generator only
+    cfg = CFG5
     nnz = args.nnz or cfg["nnz"]
-    t = DeviceCoo.generate(cfg["shape"], nnz, zipf_s=cfg["zipf_s"], normal_vals=True, seed=cfg["seed"])
-    x = uniform_vector(cfg["shape"][2], cfg["xseed"]).cpu().numpy()
-    subs, vals = sample_prefix(t, args.cpu_sample)
-    del t
-    torch.cuda.empty_cache()
-    times = []
-    kind = "port"
-    ncpu, aff = cpu_info()
+    shape, k = cfg["shape"], cfg["k"]
+    ncpu, threads = cpu_info()
+    t0 = time.perf_counter()
+    subs, vals = oracle.gen_coo(shape, nnz, zipf_s=cfg["zipf_s"], normal_vals=True, seed=cfg["seed"],
+                                threads=threads)
+    gen_s = time.perf_counter() - t0
+    x = oracle.gen_uniform(shape[k], cfg["xseed"])
+    times, parts, kind = [], None, "port"
     for i in range(args.warmup + args.steps):
-        el, kind, _ = cpu_reference_ttv_threads(subs, vals, cfg["shape"], x, cfg["k"], aff)
+        parts = None
+        parts, el, kind = oracle.ttv_raw_threads(subs, vals, shape, x, k, threads)
         if i >= args.warmup:
             times.append(el)
+    res = oracle.result_digest(parts)
+    parts = None
+    # one thread, one call (the reference's own self-timed ttv_timed) on a key-aligned prefix
+    single = None
+    ck = oracle.reference_module()
+    if ck is not None:
+        cut = oracle.shard_bounds(subs, 2, 8)[1]
+        (_, _, _), el1 = ck.ttv_timed(subs[:cut], vals[:cut], shape, x, k)
+        single = {"value": cut / el1, "unit": "nnz/s", "cores": 1, "seconds": el1,
+                  "sample": f"first {cut} rows (1/8 of the tensor, cut at a key change), one ttv_timed call"}
     ms = 1e3 * float(np.mean(times))
-    value = subs.shape[0] / (ms / 1e3)
+    value = nnz / (ms / 1e3)
     line = {
-        "impl": "reference", "metric": "sparse TTV throughput (config 5, skewed Zipf 4e8 nnz)",
-        "value": value, "unit": "nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, seeded)",
-        "config": {"workload": "cfg5_ttv_zipf_1e6x1e5x1e4_nnz4e8_mode2", "sample_rows": int(subs.shape[0]),
-                   "l2": "inputs larger than L2"},
-        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": aff, "kind": kind,
-                         "sample": f"canonical prefix of the config-5 tensor, {subs.shape[0]} rows, cut at a key change; "
-                                   f"{aff} key-aligned shards on {aff} threads (ttv_raw with release_gil=True)",
-                         "host_cpus": ncpu, "affinity": aff},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (host twin of the device generator, seeded; byte-identical tensor)",
+        "config": {"workload": WORKLOAD, "nnz": nnz, "shape": list(shape), "mode": k, "same_config": nnz == cfg["nnz"],
+                   "gen_seconds": round(gen_s, 1), "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": kind,
+                         "sample": f"the full config-5 tensor ({nnz} rows) every step: {threads} key-aligned "
+                                   f"shards on {threads} threads, ttv_raw(..., release_gil=True) each",
+                         "host_cpus": ncpu, "affinity": threads, "single_core": single},
+        "result": res,
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ---- our arm ---------------------------------------------------------------------------------
+# ---- our arm: parity and CPU baselines (oracle = checker / baseline only) -----------------------
 
-def secondary_measurements(rank, steps):
-    """Configs 1-4 on one GPU (kernel time by CUDA events, L2 flushed between iterations by writing
-    and then reading a 256 MB buffer)."""
+def host_tensor(t):
+    """Row-major (nnz, d) int64 subs and float64 vals of a DeviceCoo, on the host (pageable)."""
     import torch
+    subs = torch.stack(t.cols, dim=1).cpu().numpy()
+    return np.ascontiguousarray(subs), t.vals.cpu().numpy()
+
+
+def parity_cfg5(subs_h, vals_h, shape, xh, k, gpu_subs, gpu_vals, threads):
+    """The full config-5 result of the GPU against the reference's own kernel (oracle/_ref) on
+    the same tensor, bit for bit; the reference run is also the full-size CPU baseline."""
+    from oracle import oracle
+    parts, el, kind = oracle.ttv_raw_threads(subs_h, vals_h, shape, xh, k, threads)
+    ok = oracle.compare_parts(parts, gpu_subs, gpu_vals)
+    u_ref = sum(len(p[1]) for p in parts)
+    return {"rows": int(subs_h.shape[0]), "u": u_ref, "bit_exact": bool(ok), "checked_against": kind,
+            "seconds": el, "threads": threads}
+
+
+def harness_baselines(threads):
+    """Configs 1-3 through the reference's own harness (oracle/_ref: tenkern.run_experiment with
+    its operand schedule, 30 measured trials + 1 warm-up): ``native-loop`` (the compiled kernels,
+    one core), ``host-vectorized`` (tenhost's numpy TTV, config 3, 3 trials) and ``b200`` (this
+    package registered in the same registry, so operands and clocks are the reference's)."""
+    from oracle import oracle
+    if oracle.reference_module() is None or not os.path.isdir(os.path.join(oracle.REF_DIR, "tenhost")):
+        return None
+    import tenkern
+    from paper_2510_01495_b200 import registry
+    registry.register()
+    out = {}
+    plan = [("cfg1_dot", tenkern.ExperimentConfig("dot", sizes=(10**6,), n_trials=30), ["native-loop", "b200"]),
+            ("cfg2_matvec", tenkern.ExperimentConfig("matvec_square", sizes=(4096,), n_trials=30),
+             ["native-loop", "b200"]),
+            ("cfg3_ttv", tenkern.ExperimentConfig("ttv", sizes=(1000,), density=0.001, mode=3, n_trials=30),
+             ["native-loop", "b200"]),
+            ("cfg3_ttv_vectorized", tenkern.ExperimentConfig("ttv", sizes=(1000,), density=0.001, mode=3,
+                                                             n_trials=3), ["host-vectorized"])]
+    for name, cfg, labels in plan:
+        recs = tenkern.run_experiment(cfg, labels)
+        for s in tenkern.summarize(recs):
+            out.setdefault(name, {})[s.implementation] = {"mean_s": s.mean_s, "sd_s": s.sd_s, "n": s.n,
+                                                          "cores": 1 if s.implementation != "b200" else None}
+    return out
+
+
+def secondary_measurements(rank, steps, threads, with_cpu):
+    """Configs 1-4 on one GPU (kernel time by CUDA events, L2 flushed between iterations by
+    writing and then reading a 256 MB buffer), each with its parity against the reference's own
+    kernels (oracle/_ref) on the same operands and, with ``with_cpu``, its CPU baseline."""
+    import torch
+    from oracle import oracle
     from paper_2510_01495_b200 import _lib, synth
     from paper_2510_01495_b200 import device as dv
     from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
     lib = _lib.load()
+    ck = oracle.reference_module()
     flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")  # 256 MB > 126 MB L2
     flush_sink = torch.empty((), dtype=torch.float64, device="cuda")
     res = {}
@@ -303,17 +340,30 @@ def secondary_measurements(rank, steps):
                 ts.append(lib.tk_last_kernel_ms())
         return float(np.median(ts))
 
+    def rel_err(got, exp):
+        got, exp = np.asarray(got, dtype=np.float64), np.asarray(exp, dtype=np.float64)
+        nz = exp != 0
+        if not np.array_equal(got[~nz], exp[~nz]):
+            return float("inf")
+        return float(np.max(np.abs(got[nz] - exp[nz]) / np.abs(exp[nz]))) if nz.any() else 0.0
+
     ops = synth.host_operands(1)
     x, y = torch.from_numpy(ops["x"]).cuda(), torch.from_numpy(ops["y"]).cuda()
     out = torch.empty(1, dtype=torch.float64, device="cuda")
     ms = kernel_ms(lambda: dv.dot(x, y, out))
     res["cfg1_dot"] = {"kernel_ms": ms, "GBps": 16e6 / ms / 1e6, "bytes": 16_000_000}
+    if ck is not None:
+        res["cfg1_dot"]["parity"] = {"max_rel_err": rel_err([out.item()], [ck.dot(ops["x"], ops["y"])]),
+                                     "tol": 1e-12, "checked_against": "reference"}
     ops = synth.host_operands(2)
     a, xv = torch.from_numpy(ops["a"]).cuda(), torch.from_numpy(ops["x"]).cuda()
     yv = torch.empty(4096, dtype=torch.float64, device="cuda")
     ms = kernel_ms(lambda: dv.matvec(a, xv, yv))
     b = 8 * (4096 * 4096 + 4096 + 4096)
     res["cfg2_matvec"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "bytes": b}
+    if ck is not None:
+        res["cfg2_matvec"]["parity"] = {"max_rel_err": rel_err(yv.cpu().numpy(), ck.matvec(ops["a"], ops["x"])),
+                                        "tol": 1e-12, "checked_against": "reference"}
     ops = synth.host_operands(3)
     t3 = ops["tensor"]
     dt = DeviceCoo.from_host(t3.subs, t3.vals, t3.shape)
@@ -327,6 +377,12 @@ def secondary_measurements(rank, steps):
     ms = kernel_ms(run3)
     b = t3.nnz * 32 + 8 * 1000 + u[0] * 24
     res["cfg3_ttv"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": t3.nnz / ms * 1e3, "bytes": b, "u": u[0]}
+    if ck is not None:
+        es, ev, _ = ck.ttv_raw(t3.subs, t3.vals, t3.shape, ops["x"], 2)
+        res["cfg3_ttv"]["parity"] = {
+            "bit_exact": bool(np.array_equal(es, o_s[:u[0]].cpu().numpy())
+                              and np.array_equal(ev.view(np.int64), o_v[:u[0]].cpu().numpy().view(np.int64))),
+            "u": int(len(ev)), "checked_against": "reference"}
     del dt, o_s, o_v
     c4 = CFG4
     t4 = DeviceCoo.generate(c4["shape"], c4["nnz"], seed=c4["seed"])
@@ -335,6 +391,19 @@ def secondary_measurements(rank, steps):
     ms = kernel_ms(lambda: t4.ttv_dense(vecs, 0, out4))
     b = c4["nnz"] * 40 + 3 * 8 * 20000 + 8 * 20000
     res["cfg4_ttv_dense"] = {"kernel_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c4["nnz"] / ms * 1e3, "bytes": b}
+    if with_cpu:
+        # full-size parity: the chain of the reference's ttv_raw (modes 3, 2, 1) on every host
+        # thread (keep-mode shards), densified -- the SURVEY 8c config-4 oracle; its time is the
+        # config-4 CPU baseline
+        s4, v4 = host_tensor(t4)
+        vh = {m: vecs[m].cpu().numpy() for m in vecs}
+        ref4, el4, kind4 = oracle.ttv_multi_dense_threads(s4, v4, c4["shape"], vh, 0, threads)
+        res["cfg4_ttv_dense"]["parity"] = {"rows": int(c4["nnz"]), "max_rel_err": rel_err(out4.cpu().numpy(), ref4),
+                                           "tol": 1e-12, "checked_against": kind4 + " (chained ttv_raw)"}
+        res["cfg4_ttv_dense"]["cpu_baseline"] = {"value": c4["nnz"] / el4, "unit": "nnz/s", "cores": threads,
+                                                 "kind": kind4, "seconds": el4,
+                                                 "sample": "full tensor, chained ttv_raw on key-aligned shards"}
+        del s4, v4
     # extension (not a BASELINE config): MTTKRP of the config-4 tensor, mode 0,
     # rank 16; bytes = the stream + factor matrices + output (the R-wide gathers hit L2)
     R = 16
@@ -357,6 +426,7 @@ def secondary_measurements(rank, steps):
     o_s5 = torch.empty((t5.nnz, 2), dtype=torch.int64, device="cuda")
     o_v5 = torch.empty(t5.nnz, dtype=torch.float64, device="cuda")
     ts, u5 = [], 0
+    l0 = lib.tk_launch_count()
     for i in range(3 + 2):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -369,7 +439,7 @@ def secondary_measurements(rank, steps):
     ms = float(np.median(ts))
     b = c5["nnz"] * 32 + 8 * c5["shape"][1] + u5 * 24
     res["cfg5_ttv_mode1_sort_path"] = {"call_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c5["nnz"] / ms * 1e3,
-                                       "bytes": b, "u": u5}
+                                       "bytes": b, "u": u5, "launches_per_call": (lib.tk_launch_count() - l0) / 5}
     del t5, o_s5, o_v5
     torch.cuda.empty_cache()
     return res
@@ -403,7 +473,7 @@ def multi_dense_measurement(rank, world, steps, warmup):
     def nccl_step():
         t.ttv_dense(vecs, 0, red)
         if dist.get_backend() == "nccl":
-            dist.all_reduce(red)
+            multi.merge_dense(red)
         else:  # path check under gloo: the same sum through the host
             red.copy_(multi.merge_dense(red.cpu()))
 
@@ -437,6 +507,7 @@ def run_ours(args):
     cfg = dict(CFG5)
     nnz_total = args.nnz or cfg["nnz"]
     shape, k = cfg["shape"], cfg["k"]
+    ncpu, threads = cpu_info()
 
     # ---- operands (outside the timed region) ----
     t_gen = time.perf_counter()
@@ -448,9 +519,6 @@ def run_ours(args):
     del key
     lo, hi = bounds[rank], bounds[rank + 1]
     t = full.slice(lo, hi, copy=True) if world > 1 else full
-    cpu_leg = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        subs_s, vals_s = sample_prefix(full, args.cpu_sample)
     if world > 1:
         del full
     torch.cuda.empty_cache()
@@ -513,46 +581,61 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        if tj.get("nnz") == n_local and tj.get("kernel") == "ttv_tile_kernel<Raw,2,768,32>":
+        if tj.get("nnz") == n_local and tj.get("kernel", "").startswith("ttv_tile_kernel"):
             traffic = tj.get("dram_bytes_per_launch")
 
-    # ---- e2e through the host-buffer C ABI (pinned host in, host out) ----
+    # ---- host copies of the tensor and of the GPU result (outside every timed region) ----
+    need_host = rank == 0 and world == 1 and not (args.no_cpu and args.no_e2e)
+    subs_h = vals_h = None
+    if need_host:
+        subs_h, vals_h = host_tensor(t)
+    xh = x.cpu().numpy()
+    gpu_subs = out_subs[:u_local].cpu().numpy()
+    gpu_vals = out_vals[:u_local].cpu().numpy()
+    result = digest(gpu_subs, gpu_vals) if rank == 0 and world == 1 else None
+    if world == 1:
+        del out_subs, out_vals
+        torch.cuda.empty_cache()
+
+    # ---- e2e through the drop-in API: kernels().ttv_raw on the pageable numpy arrays a reference
+    #      caller holds (H2D of the tensor, TTV, D2H of the result, host reassembly) ----
     e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(t, x, k, args, world)
+    if not args.no_e2e and subs_h is not None:
+        e2e = run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals)
+
+    parity = None
+    cpu_leg = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        parity = parity_cfg5(subs_h, vals_h, shape, xh, k, gpu_subs, gpu_vals, threads)
+        cpu_leg = {"value": nnz_total / parity["seconds"], "unit": "nnz/s", "cores": threads,
+                   "kind": parity["checked_against"],
+                   "sample": f"the full config-5 tensor ({nnz_total} rows, same_config): {threads} key-aligned "
+                             f"shards on {threads} threads, the reference's ttv_raw(..., release_gil=True) each",
+                   "host_cpus": ncpu, "affinity": threads, "seconds": parity["seconds"]}
 
     secondary = None
     if rank == 0 and world == 1 and not args.no_secondary:
-        del out_subs, out_vals
+        del subs_h, vals_h, gpu_subs, gpu_vals, t, full
         torch.cuda.empty_cache()
-        secondary = secondary_measurements(rank, max(3, min(args.steps, 10)))
+        secondary = secondary_measurements(rank, max(3, min(args.steps, 10)), threads, not args.no_cpu)
+        if not args.no_cpu:
+            secondary["harness"] = harness_baselines(threads)
 
     multi_dense = None
     if world > 1 and not args.no_secondary:
-        del out_subs, out_vals
+        del out_subs, out_vals, t
         torch.cuda.empty_cache()
         multi_dense = multi_dense_measurement(rank, world, max(3, min(args.steps, 10)), 3)
 
-    if rank == 0 and world == 1 and not args.no_cpu:
-        xh = x.cpu().numpy()
-        el1, kind, _ = cpu_reference_ttv(subs_s, vals_s, shape, xh, k)
-        aff = cpu_info()[1]
-        el, kind, _ = cpu_reference_ttv_threads(subs_s, vals_s, shape, xh, k, aff)
-        cpu_leg = {"value": subs_s.shape[0] / el, "unit": "nnz/s", "cores": aff, "kind": kind,
-                   "sample": f"canonical prefix of the config-5 tensor, {subs_s.shape[0]} rows "
-                             f"(cut at a key change), {aff} key-aligned shards on {aff} threads",
-                   "host_cpus": cpu_info()[0], "affinity": aff, "seconds": el,
-                   "single_core": {"value": subs_s.shape[0] / el1, "cores": 1, "seconds": el1}}
-
     if rank == 0:
         line = {
-            "metric": "sparse TTV throughput (config 5, skewed Zipf 4e8 nnz)",
-            "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (device-generated, seeded; Zipf(1.2) coords, N(0,1) vals)",
-            "config": {"workload": "cfg5_ttv_zipf_1e6x1e5x1e4_nnz4e8_mode2", "nnz": nnz_total, "shape": shape,
-                       "mode": k, "u": u_total, "parallelism": f"nnz-shard{world}",
-                       "l2": "inputs (12.8 GB) larger than L2; no flush", "gen_seconds": round(gen_s, 2)},
+            "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated, seeded; Zipf(1.2) coords, N(0,1) vals)",
+            "config": {"workload": WORKLOAD, "nnz": nnz_total, "shape": list(shape), "mode": k, "u": u_total,
+                       "parallelism": f"nnz-shard{world}", "l2": "inputs (12.8 GB) larger than L2; no flush",
+                       "gen_seconds": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "frac_vs_nominal_8000": achieved / 8000.0,
@@ -562,6 +645,8 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "e2e": e2e,
             "cpu_baseline": cpu_leg,
+            "parity": parity,
+            "result": result,
             "secondary": secondary,
         }
         if multi_dense is not None:
@@ -573,40 +658,34 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(t, x, k, args, world):
-    """Host-buffer path: tk_ttv_f64_host with pinned inputs/outputs, copies timed."""
-    import ctypes
-    import torch
+def run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals):
+    """The reference caller's call: ``kernels().ttv_raw(subs, vals, shape, x, k)`` with the
+    pageable, read-only numpy arrays a SparseCooTensor holds (pkg/src/tenkern/sparse.py:101-107),
+    timed from the host (copies in and out, GPU work and the fresh output arrays inside)."""
+    import paper_2510_01495_b200 as tk
     from paper_2510_01495_b200 import _lib
-    lib = _lib.load()
-    n = t.nnz
-    subs_h = torch.empty((n, 3), dtype=torch.int64, pin_memory=True)
-    subs_h.copy_(torch.stack(t.cols, dim=1))
-    vals_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    vals_h.copy_(t.vals.cpu())
-    x_h = x.cpu().pin_memory()
-    os_h = torch.empty((n, 2), dtype=torch.int64, pin_memory=True)
-    ov_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    u = ctypes.c_int64(0)
-    shp = _lib.i64_array(t.shape)
-
-    def call():
-        _lib.check(lib.tk_ttv_f64_host(3, shp, n, subs_h.data_ptr(), vals_h.data_ptr(), x_h.data_ptr(),
-                                       int(x_h.shape[0]), k, os_h.data_ptr(), ov_h.data_ptr(), ctypes.byref(u)))
-
-    call()
+    K = tk.kernels()
+    subs_h.flags.writeable = False
+    vals_h.flags.writeable = False
+    res = K.ttv_raw(subs_h, vals_h, shape, xh, k)
+    same = bool(np.array_equal(res[0], gpu_subs) and np.array_equal(res[1].view(np.int64), gpu_vals.view(np.int64)))
+    del res
     steps = max(1, min(args.e2e_steps, args.steps))
-    barrier(world)
-    t0 = time.perf_counter()
+    ts, native = [], []
     for _ in range(steps):
-        call()
-    el = (time.perf_counter() - t0) / steps
-    el = max_over_ranks(el, world)
-    total = n * world if world == 1 else None
-    nnz_total = args.nnz or CFG5["nnz"]
-    return {"value": nnz_total / el, "unit": "nnz/s", "h2d_bytes_per_step": int(n * 32 + 8 * x_h.shape[0]),
-            "d2h_bytes_per_step": int(u.value * 24), "ms_per_step": el * 1e3, "steps": steps,
-            "path": "tk_ttv_f64_host (pinned host row-major subs/vals; key-aligned 16M-row chunks, H2D / TTV / D2H overlapped on three streams)"}
+        t0 = time.perf_counter()
+        res = K.ttv_raw(subs_h, vals_h, shape, xh, k)
+        ts.append(time.perf_counter() - t0)
+        native.append(_lib.load().tk_last_call_seconds())
+        u = len(res[1])
+        del res
+    el = float(np.mean(ts))
+    n = subs_h.shape[0]
+    return {"value": n / el, "unit": "nnz/s", "h2d_bytes_per_step": int(n * 32 + 8 * xh.shape[0]),
+            "d2h_bytes_per_step": int(u * 24), "ms_per_step": el * 1e3, "native_ms_per_step": 1e3 * float(np.mean(native)),
+            "steps": steps, "result_matches_device_path": same,
+            "path": "kernels().ttv_raw(subs, vals, shape, x, k) on pageable read-only numpy arrays "
+                    "(the reference's kernel-module call) -> tk_ttv_f64_host"}
 
 
 def main():
@@ -616,8 +695,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nnz", type=int, default=0, help="override config-5 nnz (debug only)")
-    ap.add_argument("--cpu-sample", type=int, default=320_000_000,
-                    help="rows of the config-5 prefix the CPU legs time (~10 s per call)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -625,8 +702,14 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return run_reference(args)
+    if world > 1 and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.gpus > 1 and world == 1:
+        return launch_ranks(args)
     return run_ours(args)
 
 

@@ -194,3 +194,161 @@ def reference_module():
     except ImportError:
         return None
     return ck
+
+
+# -- host twin of the device generator (oracle/tk_gen_host.cpp) ---------------------------------
+
+GEN_LIB_PATH = os.path.join(HERE, "libtk_gen_host.so")
+_gen = None
+
+
+def gen_lib():
+    global _gen
+    if _gen is None:
+        if not os.path.exists(GEN_LIB_PATH):
+            build()
+        L = ctypes.CDLL(GEN_LIB_PATH)
+        c_dp = ctypes.POINTER(ctypes.c_double)
+        c_ip = ctypes.POINTER(ctypes.c_int64)
+        L.tkg_gen_coo.restype = ctypes.c_int
+        L.tkg_gen_coo.argtypes = [ctypes.c_int, c_ip, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
+                                  ctypes.c_uint64, ctypes.c_int, c_ip, c_dp]
+        L.tkg_gen_uniform.restype = None
+        L.tkg_gen_uniform.argtypes = [ctypes.c_int64, ctypes.c_uint64, c_dp]
+        L.tkg_zipf_cdf.restype = None
+        L.tkg_zipf_cdf.argtypes = [ctypes.c_int64, ctypes.c_double, c_dp]
+        L.tkg_ln.restype = ctypes.c_double
+        L.tkg_ln.argtypes = [ctypes.c_double]
+        L.tkg_cos2pi.restype = ctypes.c_double
+        L.tkg_cos2pi.argtypes = [ctypes.c_double]
+        L.tkg_shard_bounds.restype = None
+        L.tkg_shard_bounds.argtypes = [c_ip, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_ip]
+        _gen = L
+    return _gen
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def gen_coo(shape, nnz: int, *, zipf_s: float = 0.0, normal_vals: bool = False, seed: int = 12345,
+            threads: int = 0):
+    """Exact-nnz tensor of the device generator (tk_gen.cu gen_coo), built on the host:
+    row-major canonical subs (nnz, d) int64 and float64 vals, byte-identical to
+    ``DeviceCoo.generate(shape, nnz, zipf_s=..., normal_vals=..., seed=...)``."""
+    shape = tuple(int(s) for s in shape)
+    d = len(shape)
+    subs = np.empty((nnz, d), dtype=np.int64)
+    vals = np.empty(nnz, dtype=np.float64)
+    shp = np.asarray(shape, dtype=np.int64)
+    rc = gen_lib().tkg_gen_coo(d, _ip(shp), int(nnz), float(zipf_s), int(bool(normal_vals)),
+                               int(seed) & (2**64 - 1), int(threads or host_threads()), _ip(subs), _dp(vals))
+    if rc != 0:
+        raise ValueError(f"gen_coo: bad arguments (rc={rc})")
+    return subs, vals
+
+
+def gen_uniform(n: int, seed: int) -> np.ndarray:
+    """The device's seeded uniform vector (tk_gen.cu uniform_kernel), on the host."""
+    out = np.empty(int(n), dtype=np.float64)
+    gen_lib().tkg_gen_uniform(int(n), int(seed) & (2**64 - 1), _dp(out))
+    return out
+
+
+def shard_bounds(subs, nkeep: int, parts: int) -> list:
+    """Split points of row-major canonical ``subs`` into ``parts`` ranges, each moved forward to
+    the next change of the first ``nkeep`` columns (no output group spans two ranges)."""
+    subs = np.ascontiguousarray(subs, dtype=np.int64)
+    b = np.empty(parts + 1, dtype=np.int64)
+    gen_lib().tkg_shard_bounds(_ip(subs), subs.shape[0], subs.shape[1], int(nkeep), int(parts), _ip(b))
+    return [int(v) for v in b]
+
+
+def ttv_raw_threads(subs, vals, shape, x, k, threads: int = 0):
+    """The reference's compiled ``ttv_raw`` (oracle/_ref; else the C port) over ``threads``
+    key-aligned shards of a canonical tensor whose contracted mode is the last one, each shard on
+    its own Python thread with the GIL released (``ttv_raw(..., release_gil=True)``,
+    _ckernels.pyx:370-374).  The rank-order concatenation is the one-call result.  Returns
+    ((subs, vals, shape), seconds, kind)."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+    threads = int(threads or host_threads())
+    ck = reference_module()
+    kind = "reference" if ck is not None else "port"
+    d = len(shape)
+    bounds = shard_bounds(subs, d - 1, threads)
+
+    def run(i):
+        lo, hi = bounds[i], bounds[i + 1]
+        if ck is not None:
+            return ck.ttv_raw(subs[lo:hi], vals[lo:hi], tuple(shape), x, k, True)
+        return ttv_raw(subs[lo:hi], vals[lo:hi], shape, x, k)
+    with ThreadPoolExecutor(threads) as ex:
+        t0 = time.perf_counter()
+        parts = list(ex.map(run, range(threads)))
+        el = time.perf_counter() - t0
+    return parts, el, kind
+
+
+def result_digest(parts) -> dict:
+    """sha256 of the concatenated (subs, vals) bytes of a TTV result given as a list of
+    (subs, vals, shape) parts in order (one part = a whole result).  Row-major int64 subs and
+    float64 vals: the reference's TtvRawResult layout, so GPU and CPU results hash alike."""
+    import hashlib
+    hs, hv = hashlib.sha256(), hashlib.sha256()
+    u = 0
+    for s, v, _ in parts:
+        hs.update(np.ascontiguousarray(s, dtype=np.int64).data)
+        hv.update(np.ascontiguousarray(v, dtype=np.float64).data)
+        u += len(v)
+    return {"u": u, "subs_sha256": hs.hexdigest(), "vals_sha256": hv.hexdigest()}
+
+
+def compare_parts(parts, subs, vals) -> bool:
+    """Bitwise equality of a result given as ordered parts with one contiguous result."""
+    off = 0
+    for s, v, _ in parts:
+        n = len(v)
+        if not np.array_equal(np.asarray(s).reshape(n, -1), subs[off:off + n].reshape(n, -1)):
+            return False
+        if not np.array_equal(np.asarray(v).view(np.int64), np.asarray(vals[off:off + n]).view(np.int64)):
+            return False
+        off += n
+    return off == len(vals)
+
+
+def ttv_multi_dense_threads(subs, vals, shape, vecs: dict, keep: int = 0, threads: int = 0):
+    """``ttv_multi_dense`` on every host thread: canonical input with ``keep == 0`` is cut into
+    key-aligned shards of the keep mode (no keep index spans two shards), each shard runs the
+    chain of the reference's ``ttv_raw`` (oracle/_ref, GIL released; else the C port) and
+    densifies into its own disjoint part of the output.  Returns (out, seconds, kind)."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+    if keep != 0:
+        raise ValueError("ttv_multi_dense_threads: keep must be 0 (canonical order sorts mode 0)")
+    threads = int(threads or host_threads())
+    ck = reference_module()
+    kind = "reference" if ck is not None else "port"
+    d = len(shape)
+    bounds = shard_bounds(subs, 1, threads)
+    out = np.zeros(shape[keep], dtype=np.float64)
+
+    def run(i):
+        lo, hi = bounds[i], bounds[i + 1]
+        if hi <= lo:
+            return
+        cs, cv, csh = subs[lo:hi], vals[lo:hi], tuple(shape)
+        for m in sorted((m for m in range(d) if m != keep), reverse=True):
+            if ck is not None:
+                cs, cv, csh = ck.ttv_raw(cs, cv, csh, vecs[m], m, True)
+            else:
+                cs, cv, csh = ttv_raw(cs, cv, csh, vecs[m], m)
+        out[np.asarray(cs)[:, 0]] = cv
+    with ThreadPoolExecutor(threads) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(run, range(threads)))
+        el = time.perf_counter() - t0
+    return out, el, kind

@@ -102,7 +102,12 @@ def _ttv_host(subs, vals, shape, x, k):
                                             xv.shape[0], k, out_subs.ctypes.data, out_vals.ctypes.data,
                                             ctypes.byref(u)))
     n = u.value
-    return out_subs[:n].copy(), out_vals[:n].copy(), new_shape
+    # fresh, owned, exact-size outputs like the reference's copy-out (pyx:367), without a second
+    # host copy: the capacity-sized buffers are shrunk in place (realloc; pages past u were never
+    # touched, so they were never committed)
+    out_subs.resize((n, d - 1), refcheck=False)
+    out_vals.resize((n,), refcheck=False)
+    return out_subs, out_vals, new_shape
 
 
 def ttv_raw(subs, vals, shape, x, k, release_gil=False):

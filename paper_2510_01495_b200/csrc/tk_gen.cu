@@ -107,6 +107,83 @@ struct ColPtrs {
   long long* col[kMaxOrder];
 };
 
+// ---- N(0,1) values from exactly-rounded operations only -----------------------------------
+// Box-Muller with its own ln and cos built from IEEE +, -, *, / and sqrt, each an explicit
+// round-to-nearest intrinsic (no FMA contraction, no libdevice approximation).  The host twin of
+// this generator (oracle/tk_gen_host.cpp) performs the same operation sequence, so device- and
+// host-generated tensors are byte-identical (tests/test_gen_twin.py).
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+
+// ln(x), x in [2^-53, 1]: x = 2^e m, m in [sqrt(1/2), sqrt(2)); ln m = 2 atanh(f) with
+// f = (m - 1) / (m + 1) (|f| <= 0.172), odd series to f^23.
+__device__ double gen_ln(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  int e = (int)((b >> 52) & 0x7ff) - 1023;
+  double m = __longlong_as_double((long long)((b & 0xFFFFFFFFFFFFFull) | (1023ull << 52)));
+  if (m > 0x1.6a09e667f3bcdp+0) {
+    m = rn_mul(m, 0.5);
+    e += 1;
+  }
+  const double f = __ddiv_rn(rn_sub(m, 1.0), rn_add(m, 1.0));
+  const double s = rn_mul(f, f);
+  double q = 0x1.642c8590b2164p-5;                  // 1/23
+  q = rn_add(0x1.8618618618618p-5, rn_mul(s, q));   // 1/21
+  q = rn_add(0x1.af286bca1af28p-5, rn_mul(s, q));   // 1/19
+  q = rn_add(0x1.e1e1e1e1e1e1ep-5, rn_mul(s, q));   // 1/17
+  q = rn_add(0x1.1111111111111p-4, rn_mul(s, q));   // 1/15
+  q = rn_add(0x1.3b13b13b13b14p-4, rn_mul(s, q));   // 1/13
+  q = rn_add(0x1.745d1745d1746p-4, rn_mul(s, q));   // 1/11
+  q = rn_add(0x1.c71c71c71c71cp-4, rn_mul(s, q));   // 1/9
+  q = rn_add(0x1.2492492492492p-3, rn_mul(s, q));   // 1/7
+  q = rn_add(0x1.999999999999ap-3, rn_mul(s, q));   // 1/5
+  q = rn_add(0x1.5555555555555p-2, rn_mul(s, q));   // 1/3
+  const double f2 = rn_add(f, f);
+  const double lm = rn_add(f2, rn_mul(rn_mul(f2, s), q));
+  return rn_add(rn_mul((double)e, 0x1.62e42fefa39efp-1), lm);  // e ln 2 + ln m
+}
+
+// cos y and sin y for y in [0, pi/4]: Taylor to y^16 / y^17, Horner in z = y^2
+__device__ double gen_cos_q(double y) {
+  const double z = rn_mul(y, y);
+  double q = 0x1.ae7f3e733b81fp-45;                 // 1/16!
+  q = rn_sub(0x1.93974a8c07c9dp-37, rn_mul(z, q));  // 1/14!
+  q = rn_sub(0x1.1eed8eff8d898p-29, rn_mul(z, q));  // 1/12!
+  q = rn_sub(0x1.27e4fb7789f5cp-22, rn_mul(z, q));  // 1/10!
+  q = rn_sub(0x1.a01a01a01a01ap-16, rn_mul(z, q));  // 1/8!
+  q = rn_sub(0x1.6c16c16c16c17p-10, rn_mul(z, q));  // 1/6!
+  q = rn_sub(0x1.5555555555555p-5, rn_mul(z, q));   // 1/4!
+  q = rn_sub(0.5, rn_mul(z, q));                    // 1/2!
+  return rn_sub(1.0, rn_mul(z, q));
+}
+__device__ double gen_sin_q(double y) {
+  const double z = rn_mul(y, y);
+  double q = 0x1.952c77030ad4ap-49;                 // 1/17!
+  q = rn_sub(0x1.ae7f3e733b81fp-41, rn_mul(z, q));  // 1/15!
+  q = rn_sub(0x1.6124613a86d09p-33, rn_mul(z, q));  // 1/13!
+  q = rn_sub(0x1.ae64567f544e4p-26, rn_mul(z, q));  // 1/11!
+  q = rn_sub(0x1.71de3a556c734p-19, rn_mul(z, q));  // 1/9!
+  q = rn_sub(0x1.a01a01a01a01ap-13, rn_mul(z, q));  // 1/7!
+  q = rn_sub(0x1.1111111111111p-7, rn_mul(z, q));   // 1/5!
+  q = rn_sub(0x1.5555555555555p-3, rn_mul(z, q));   // 1/3!
+  return rn_sub(y, rn_mul(rn_mul(y, z), q));
+}
+
+// cos(2 pi t), t in [0, 1): exact reductions (Sterbenz) to t in [0, 1/8] or [1/8, 1/4], then the
+// cosine or sine polynomial
+__device__ double gen_cos2pi(double t) {
+  double sign = 1.0;
+  if (t > 0.5) t = rn_sub(1.0, t);
+  if (t > 0.25) {
+    t = rn_sub(0.5, t);
+    sign = -1.0;
+  }
+  const double c = t > 0.125 ? gen_sin_q(rn_mul(0x1.921fb54442d18p+2, rn_sub(0.25, t)))
+                             : gen_cos_q(rn_mul(0x1.921fb54442d18p+2, t));
+  return rn_mul(sign, c);
+}
+
 __global__ void unravel_vals_kernel(GenParams p, long long n, const unsigned long long* __restrict__ keys,
                                     int normal_vals, ColPtrs cp, double* __restrict__ vals) {
   const uint2 vk = make_uint2(p.key.x ^ (unsigned)kValSalt, p.key.y ^ (unsigned)(kValSalt >> 32));
@@ -124,9 +201,9 @@ __global__ void unravel_vals_kernel(GenParams p, long long n, const unsigned lon
       if (!normal_vals) {
         v = u53(c.x, c.y);
       } else {
-        const double u1 = 1.0 - u53(c.x, c.y);  // (0, 1]
+        const double u1 = rn_sub(1.0, u53(c.x, c.y));  // (0, 1], exact
         const double u2 = u53(c.z, c.w);
-        v = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        v = rn_mul(__dsqrt_rn(rn_mul(-2.0, gen_ln(u1))), gen_cos2pi(u2));
       }
     }
     vals[t] = v;
