@@ -208,8 +208,8 @@ int tk_dot_f64_host(const double* x, const double* y, int64_t n, double* out) {
   double* dy = dx + pn;
   double* dout = dy + pn;
   if (n) {
-    TK_CUDA(cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, st));
-    TK_CUDA(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, st));
+    if (int rc = h2d(dx, x, n * 8, st)) return rc;
+    if (int rc = h2d(dy, y, n * 8, st)) return rc;
   }
   if (int rc = dot_device(dx, dy, n, dout, st)) return rc;
   double* h = static_cast<double*>(pinned_scratch(8));
@@ -238,11 +238,10 @@ int tk_matvec_f64_host(const double* a, int64_t rows, int64_t cols, const double
   double* da = b.as<double>();
   double* dx = da + pa;
   double* dy = dx + px;
-  if (na) TK_CUDA(cudaMemcpyAsync(da, a, na * 8, cudaMemcpyHostToDevice, st));
-  if (cols) TK_CUDA(cudaMemcpyAsync(dx, x, (size_t)cols * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = h2d(da, a, na * 8, st)) return rc;
+  if (int rc = h2d(dx, x, (size_t)cols * 8, st)) return rc;
   if (int rc = matvec_device(da, rows, cols, dx, dy, st)) return rc;
-  TK_CUDA(cudaMemcpyAsync(y, dy, (size_t)rows * 8, cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaStreamSynchronize(st));
+  if (int rc = d2h(y, dy, (size_t)rows * 8, st)) return rc;
   return TK_OK;
 }
 
@@ -270,7 +269,7 @@ int tk_ttv_f64_device(int32_t d, const int64_t* shape, int64_t nnz, const int64_
   return ttv_sparse_device(d, shape, nnz, cp.data(), vals, x, nx, k, out_subs, out_vals, out_nnz, st);
 }
 
-constexpr int64_t kPipeRows = 16ll << 20;  // rows per chunk of the pipelined host TTV
+constexpr int64_t kPipeRows = 8ll << 20;  // rows per chunk of the pipelined host TTV
 constexpr int kPipeDeclined = -1;          // the pipelined path does not apply: use the one-shot path
 
 cudaStream_t side_stream(int which) {  // 0: host->device copies, 1: device->host copies
@@ -289,14 +288,46 @@ int key_cmp(const int64_t* subs, int d, int64_t i, int64_t j) {
   return 0;
 }
 
+// Pinned host staging shared by the pipelined TTV calls of one device (inputs and outputs; two
+// halves each, reused across calls, grown on demand).
+struct PipeStage {
+  std::mutex mu;
+  char* in = nullptr;
+  char* out = nullptr;
+  size_t in_half = 0, out_half = 0;
+  int ensure(size_t in_b, size_t out_b) {
+    if (in_b > in_half) {
+      if (in) cudaFreeHost(in);
+      in = nullptr;
+      in_half = 0;
+      TK_CUDA(cudaMallocHost(&in, 2 * in_b));
+      in_half = in_b;
+    }
+    if (out_b > out_half) {
+      if (out) cudaFreeHost(out);
+      out = nullptr;
+      out_half = 0;
+      TK_CUDA(cudaMallocHost(&out, 2 * out_b));
+      out_half = out_b;
+    }
+    return TK_OK;
+  }
+};
+PipeStage& pipe_stage() {
+  static PipeStage s[64];
+  return s[cur_dev()];
+}
+
 // Host-buffer TTV with k == d-1, pipelined over chunks cut at kept-key changes: the copy of chunk
-// i+1 in, the TTV of chunk i and the copy of chunk i-1's result out overlap (PCIe is full duplex),
-// so the call costs ~ the input transfer.  Each chunk is a complete set of groups, so the result
-// is the concatenation of the chunk results.  Declines (kPipeDeclined) if the input is not in
-// kept-key order -- the one-shot path then sorts.
+// i+1 in, the TTV of chunk i and the copy of chunk i-1's result out overlap (PCIe is full duplex).
+// Each chunk is a complete set of groups, so the result is the concatenation of the chunk results.
+// Pinned caller buffers are DMA'd directly.  Pageable ones (the reference caller's numpy arrays)
+// go through pinned staging: the host packs chunk i+1's rows (RowPack: one 64-bit word per row
+// when every index fits its dimension, else the raw int64 rows) with the thread pool while the
+// DMA of chunk i runs, and copies chunk i-1's result out of its staging half in parallel.
+// Declines (kPipeDeclined) if the input is not in kept-key order -- the one-shot path then sorts.
 int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
                        const double* x, int64_t nx, int64_t* out_subs, double* out_vals, int64_t* out_nnz) {
-  (void)shape;
   const int nk = d - 1;
   std::vector<int64_t> cut{0};
   while (cut.back() < nnz) {
@@ -309,7 +340,19 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
   int64_t rows = 0;
   for (int i = 0; i < nchunk; ++i) rows = std::max(rows, cut[i + 1] - cut[i]);
   const int64_t pitch = pitch_of(rows);
+  const bool pin_in = host_is_pinned(subs) && host_is_pinned(vals);
+  const bool pin_out = host_is_pinned(out_subs) && host_is_pinned(out_vals);
+  RowPack rp;
+  const bool packable = !pin_in && row_pack_plan(d, shape, &rp);
   cudaStream_t sc = lib_stream(), si = side_stream(0), so = side_stream(1);
+  std::unique_lock<std::mutex> stage_lock;
+  PipeStage* ps = nullptr;
+  if (!pin_in || !pin_out) {
+    ps = &pipe_stage();
+    stage_lock = std::unique_lock<std::mutex>(ps->mu);
+    if (int rc = ps->ensure(pin_in ? 0 : (size_t)rows * (d + 1) * 8, pin_out ? 0 : (size_t)rows * (nk + 1) * 8))
+      return rc;
+  }
   DevBuf b_x, b_aos[2], b_soa[2], b_vals[2], b_os[2], b_ov[2];
   if (int rc = b_x.alloc((size_t)std::max<int64_t>(nx, 1) * 8, sc)) return rc;
   for (int b = 0; b < 2; ++b) {
@@ -345,16 +388,39 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
   TK_CUDA(cudaEventRecord(ev_done[0], sc));
   TK_CUDA(cudaStreamWaitEvent(si, ev_done[0], 0));
   TK_CUDA(cudaStreamWaitEvent(so, ev_done[0], 0));
+  bool packed[2] = {false, false};
   auto copy_in = [&](int i) -> int {
     const int b = i & 1;
     const int64_t n = cut[i + 1] - cut[i];
-    TK_CUDA(cudaMemcpyAsync(b_aos[b].get(), subs + cut[i] * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, si));
-    TK_CUDA(cudaMemcpyAsync(b_vals[b].get(), vals + cut[i], (size_t)n * 8, cudaMemcpyHostToDevice, si));
+    if (pin_in) {
+      TK_CUDA(cudaMemcpyAsync(b_aos[b].get(), subs + cut[i] * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, si));
+      TK_CUDA(cudaMemcpyAsync(b_vals[b].get(), vals + cut[i], (size_t)n * 8, cudaMemcpyHostToDevice, si));
+    } else {
+      TK_CUDA(cudaEventSynchronize(ev_in[b]));  // the DMA that last read this staging half is done
+      char* stg = ps->in + (size_t)b * ps->in_half;
+      double* sv = reinterpret_cast<double*>(stg + (size_t)rows * d * 8);
+      packed[b] = packable && pack_rows(rp, subs + cut[i] * d, vals + cut[i], n, reinterpret_cast<uint64_t*>(stg), sv);
+      if (!packed[b]) {  // an index outside its dimension (or too many bits): raw rows
+        pmemcpy(stg, subs + cut[i] * d, (size_t)n * d * 8);
+        pmemcpy(sv, vals + cut[i], (size_t)n * 8);
+      }
+      TK_CUDA(cudaMemcpyAsync(b_aos[b].get(), stg, (size_t)n * (packed[b] ? 1 : d) * 8, cudaMemcpyHostToDevice, si));
+      TK_CUDA(cudaMemcpyAsync(b_vals[b].get(), sv, (size_t)n * 8, cudaMemcpyHostToDevice, si));
+    }
     TK_CUDA(cudaEventRecord(ev_in[b], si));
     return TK_OK;
   };
+  std::vector<int64_t> offs(nchunk + 1, 0), us(nchunk, 0);
+  auto copy_out_host = [&](int i) -> int {  // pageable outputs: staging half -> caller, in parallel
+    const int b = i & 1;
+    TK_CUDA(cudaEventSynchronize(ev_free[b]));
+    const int64_t u = us[i];
+    char* stg = ps->out + (size_t)b * ps->out_half;
+    pmemcpy(out_subs + offs[i] * nk, stg, (size_t)u * nk * 8);
+    pmemcpy(out_vals + offs[i], stg + (size_t)rows * nk * 8, (size_t)u * 8);
+    return TK_OK;
+  };
   if (int rc = copy_in(0)) return rc;
-  int64_t off = 0;
   for (int i = 0; i < nchunk; ++i) {
     const int b = i & 1;
     const int64_t n = cut[i + 1] - cut[i];
@@ -363,7 +429,11 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
     }
     TK_CUDA(cudaStreamWaitEvent(sc, ev_in[b], 0));
     if (i >= 2) TK_CUDA(cudaStreamWaitEvent(sc, ev_free[b], 0));  // chunk i-2's result copied out
-    if (int rc = aos_to_soa(n, d, b_aos[b].as<int64_t>(), b_soa[b].as<int64_t>(), pitch, sc)) return rc;
+    if (packed[b] && !pin_in) {
+      if (int rc = unpack_rows(rp, n, b_aos[b].as<uint64_t>(), b_soa[b].as<int64_t>(), pitch, sc)) return rc;
+    } else {
+      if (int rc = aos_to_soa(n, d, b_aos[b].as<int64_t>(), b_soa[b].as<int64_t>(), pitch, sc)) return rc;
+    }
     std::vector<const int64_t*> cp(d);
     for (int m = 0; m < d; ++m) cp[m] = b_soa[b].as<int64_t>() + (size_t)m * pitch;
     int64_t u = 0;
@@ -372,18 +442,29 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
                                 b_ov[b].as<double>(), &u, &unsorted, sc))
       return rc;
     if (unsorted) return kPipeDeclined;
+    us[i] = u;
+    offs[i + 1] = offs[i] + u;
     TK_CUDA(cudaEventRecord(ev_done[b], sc));
     TK_CUDA(cudaStreamWaitEvent(so, ev_done[b], 0));
     if (u) {
-      TK_CUDA(cudaMemcpyAsync(out_subs + off * nk, b_os[b].get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, so));
-      TK_CUDA(cudaMemcpyAsync(out_vals + off, b_ov[b].get(), (size_t)u * 8, cudaMemcpyDeviceToHost, so));
+      if (pin_out) {
+        TK_CUDA(cudaMemcpyAsync(out_subs + offs[i] * nk, b_os[b].get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, so));
+        TK_CUDA(cudaMemcpyAsync(out_vals + offs[i], b_ov[b].get(), (size_t)u * 8, cudaMemcpyDeviceToHost, so));
+      } else {
+        char* stg = ps->out + (size_t)b * ps->out_half;
+        TK_CUDA(cudaMemcpyAsync(stg, b_os[b].get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, so));
+        TK_CUDA(cudaMemcpyAsync(stg + (size_t)rows * nk * 8, b_ov[b].get(), (size_t)u * 8, cudaMemcpyDeviceToHost, so));
+      }
     }
     TK_CUDA(cudaEventRecord(ev_free[b], so));
-    off += u;
+    if (!pin_out && i >= 1)
+      if (int rc = copy_out_host(i - 1)) return rc;
   }
   TK_CUDA(cudaStreamSynchronize(so));
   TK_CUDA(cudaStreamSynchronize(sc));
-  *out_nnz = off;
+  if (!pin_out && nchunk >= 1)
+    if (int rc = copy_out_host(nchunk - 1)) return rc;
+  *out_nnz = offs[nchunk];
   return TK_OK;
 }
 
@@ -409,9 +490,9 @@ int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t*
   if (int rc = b_x.alloc((size_t)std::max<int64_t>(nx, 1) * 8, st)) return rc;
   if (int rc = b_os.alloc((size_t)nnz * nk * 8, st)) return rc;
   if (int rc = b_ov.alloc((size_t)nnz * 8, st)) return rc;
-  TK_CUDA(cudaMemcpyAsync(b_aos.get(), subs, (size_t)nnz * d * 8, cudaMemcpyHostToDevice, st));
-  TK_CUDA(cudaMemcpyAsync(b_vals.get(), vals, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
-  if (nx) TK_CUDA(cudaMemcpyAsync(b_x.get(), x, (size_t)nx * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = h2d(b_aos.get(), subs, (size_t)nnz * d * 8, st)) return rc;
+  if (int rc = h2d(b_vals.get(), vals, (size_t)nnz * 8, st)) return rc;
+  if (int rc = h2d(b_x.get(), x, (size_t)nx * 8, st)) return rc;
   if (int rc = aos_to_soa(nnz, d, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
   b_aos.reset();
   std::vector<const int64_t*> cp(d);
@@ -420,10 +501,8 @@ int tk_ttv_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64_t*
   if (int rc = ttv_sparse_device(d, shape, nnz, cp.data(), b_vals.as<double>(), b_x.as<double>(), nx, k,
                                  b_os.as<int64_t>(), b_ov.as<double>(), &u, st))
     return rc;
-  if (u) {
-    TK_CUDA(cudaMemcpyAsync(out_subs, b_os.get(), (size_t)u * nk * 8, cudaMemcpyDeviceToHost, st));
-    TK_CUDA(cudaMemcpyAsync(out_vals, b_ov.get(), (size_t)u * 8, cudaMemcpyDeviceToHost, st));
-  }
+  if (int rc = d2h(out_subs, b_os.get(), (size_t)u * nk * 8, st)) return rc;
+  if (int rc = d2h(out_vals, b_ov.get(), (size_t)u * 8, st)) return rc;
   TK_CUDA(cudaStreamSynchronize(st));
   *out_nnz = u;
   return TK_OK;
@@ -446,8 +525,8 @@ int tk_group_sum_f64_host(int64_t n, int32_t m, const int64_t* keys, const doubl
   if (int rc = b_os.alloc((size_t)n * m * 8, st)) return rc;
   if (int rc = b_ov.alloc((size_t)n * 8, st)) return rc;
   static const double one = 1.0;
-  TK_CUDA(cudaMemcpyAsync(b_aos.get(), keys, (size_t)n * m * 8, cudaMemcpyHostToDevice, st));
-  TK_CUDA(cudaMemcpyAsync(b_w.get(), weights, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = h2d(b_aos.get(), keys, (size_t)n * m * 8, st)) return rc;
+  if (int rc = h2d(b_w.get(), weights, (size_t)n * 8, st)) return rc;
   TK_CUDA(cudaMemcpyAsync(b_one.get(), &one, 8, cudaMemcpyHostToDevice, st));
   if (int rc = aos_to_soa(n, m, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
   TK_CUDA(cudaMemsetAsync(b_soa.as<int64_t>() + (size_t)m * pitch, 0, (size_t)n * 8, st));
@@ -461,10 +540,8 @@ int tk_group_sum_f64_host(int64_t n, int32_t m, const int64_t* keys, const doubl
   if (int rc = ttv_sparse_device(d, shape.data(), n, cp.data(), b_w.as<double>(), b_one.as<double>(), 1, m,
                                  b_os.as<int64_t>(), b_ov.as<double>(), &u, st, /*keep_zeros=*/true))
     return rc;
-  if (u) {
-    TK_CUDA(cudaMemcpyAsync(out_keys, b_os.get(), (size_t)u * m * 8, cudaMemcpyDeviceToHost, st));
-    TK_CUDA(cudaMemcpyAsync(out_sums, b_ov.get(), (size_t)u * 8, cudaMemcpyDeviceToHost, st));
-  }
+  if (int rc = d2h(out_keys, b_os.get(), (size_t)u * m * 8, st)) return rc;
+  if (int rc = d2h(out_sums, b_ov.get(), (size_t)u * 8, st)) return rc;
   TK_CUDA(cudaStreamSynchronize(st));
   *out_u = u;
   return TK_OK;
@@ -735,8 +812,8 @@ int tk_mttkrp_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64
   if (int rc = b_fac.alloc(fac_elems * 8 + 8, st)) return rc;
   if (int rc = b_out.alloc((size_t)shape[n] * rank * 8 + 8, st)) return rc;
   if (nnz) {
-    TK_CUDA(cudaMemcpyAsync(b_aos.get(), subs, (size_t)nnz * d * 8, cudaMemcpyHostToDevice, st));
-    TK_CUDA(cudaMemcpyAsync(b_vals.get(), vals, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+    if (int rc = h2d(b_aos.get(), subs, (size_t)nnz * d * 8, st)) return rc;
+    if (int rc = h2d(b_vals.get(), vals, (size_t)nnz * 8, st)) return rc;
     if (int rc = aos_to_soa(nnz, d, b_aos.as<int64_t>(), b_soa.as<int64_t>(), pitch, st)) return rc;
   }
   std::vector<const double*> fp(d, nullptr);
@@ -747,14 +824,13 @@ int tk_mttkrp_f64_host(int32_t d, const int64_t* shape, int64_t nnz, const int64
     if (m == n) continue;
     double* dst = b_fac.as<double>() + off;
     if (shape[m] > 0 && rank > 0)
-      TK_CUDA(cudaMemcpyAsync(dst, factors[m], (size_t)shape[m] * rank * 8, cudaMemcpyHostToDevice, st));
+      if (int rc = h2d(dst, factors[m], (size_t)shape[m] * rank * 8, st)) return rc;
     fp[m] = dst;
     off += (size_t)pitch_of(shape[m] * rank);
   }
   if (int rc = mttkrp_device(d, shape, nnz, cp.data(), b_vals.as<double>(), n, rank, fp.data(), b_out.as<double>(), st))
     return rc;
-  if (shape[n] > 0 && rank > 0)
-    TK_CUDA(cudaMemcpyAsync(out, b_out.get(), (size_t)shape[n] * rank * 8, cudaMemcpyDeviceToHost, st));
+  if (int rc = d2h(out, b_out.get(), (size_t)shape[n] * rank * 8, st)) return rc;
   TK_CUDA(cudaStreamSynchronize(st));
   return TK_OK;
 }

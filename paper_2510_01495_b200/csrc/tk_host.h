@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -90,6 +91,29 @@ int ttv_dense_chain(int d, const int64_t* shape, int64_t nnz, const int64_t* con
 int mttkrp_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals, int mode,
                   int64_t R, const double* const* factors, double* out, cudaStream_t st);
 int aos_to_soa(int64_t nnz, int d, const int64_t* aos, int64_t* soa, int64_t pitch, cudaStream_t st);
+
+// ---- host side of the host-buffer calls (tk_hostio.cu) ----
+int host_threads();
+void parallel_for(int n, const std::function<void(int)>& fn);  // persistent host thread pool
+void pmemcpy(void* dst, const void* src, size_t bytes);          // parallel host memcpy
+bool host_is_pinned(const void* p);
+// H2D / D2H of caller host memory: pinned -> direct DMA; pageable -> chunked through a per-device
+// pinned arena (parallel host copy of chunk i+1 overlapping the DMA of chunk i).  h2d is
+// stream-ordered (the source may be reused on return); d2h returns with the data on the host.
+int h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+int d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// Packed tensor rows: coordinate m of a row in bits [shift[m], shift[m] + bits(dim[m]-1)) of one
+// 64-bit word (only when the bit widths sum to <= 64 and every index is inside its dimension).
+struct RowPack {
+  int d;
+  int shift[TK_MAX_ORDER];
+  uint64_t dim[TK_MAX_ORDER];
+};
+bool row_pack_plan(int d, const int64_t* shape, RowPack* p);
+// packs n row-major rows and copies their values (parallel); false if some index is out of range
+bool pack_rows(const RowPack& p, const int64_t* subs, const double* vals, int64_t n, uint64_t* packed,
+               double* vals_out);
+int unpack_rows(const RowPack& p, int64_t n, const uint64_t* packed, int64_t* soa, int64_t pitch, cudaStream_t st);
 
 int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStream_t st);
 int matvec_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, cudaStream_t st);

@@ -172,12 +172,22 @@ __global__ void gather_w_kernel(long long n, const long long* __restrict__ perm,
 
 __global__ void aos_to_soa_kernel(long long n, int d, const long long* __restrict__ aos, long long* __restrict__ soa,
                                   long long pitch) {
-  const long long total = n * d;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long r = e / d;
-    const int m = (int)(e - r * d);
-    soa[m * pitch + r] = __ldcs(aos + e);
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    for (int m = 0; m < d; ++m) soa[m * pitch + r] = __ldcs(aos + r * d + m);
+}
+
+// packed host rows (tk_hostio.cu RowPack) -> SoA columns
+struct UnpackPlan {
+  int d;
+  int shift[kMaxOrder];
+  unsigned long long mask[kMaxOrder];
+};
+
+__global__ void unpack_rows_kernel(long long n, UnpackPlan p, const unsigned long long* __restrict__ packed,
+                                   long long* __restrict__ soa, long long pitch) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long w = __ldcs(packed + r);
+    for (int m = 0; m < p.d; ++m) soa[m * pitch + r] = (long long)((w >> p.shift[m]) & p.mask[m]);
   }
 }
 
@@ -1091,8 +1101,25 @@ int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* c
 
 int aos_to_soa(int64_t nnz, int d, const int64_t* aos, int64_t* soa, int64_t pitch, cudaStream_t st) {
   if (nnz == 0) return TK_OK;
-  aos_to_soa_kernel<<<grid_for(nnz * d), 256, 0, st>>>(nnz, d, reinterpret_cast<const long long*>(aos),
-                                                        reinterpret_cast<long long*>(soa), pitch);
+  aos_to_soa_kernel<<<grid_for(nnz), 256, 0, st>>>(nnz, d, reinterpret_cast<const long long*>(aos),
+                                                   reinterpret_cast<long long*>(soa), pitch);
+  count_launch();
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+int unpack_rows(const RowPack& rp, int64_t n, const uint64_t* packed, int64_t* soa, int64_t pitch, cudaStream_t st) {
+  if (n == 0) return TK_OK;
+  UnpackPlan p{};
+  p.d = rp.d;
+  for (int m = 0; m < rp.d; ++m) {
+    const uint64_t top = rp.dim[m] - 1;
+    const int bits = top == 0 ? 0 : 64 - __builtin_clzll(top);
+    p.shift[m] = rp.shift[m];
+    p.mask[m] = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+  }
+  unpack_rows_kernel<<<grid_for(n), 256, 0, st>>>(n, p, reinterpret_cast<const unsigned long long*>(packed),
+                                                  reinterpret_cast<long long*>(soa), pitch);
   count_launch();
   TK_CUDA(cudaGetLastError());
   return TK_OK;

@@ -22,6 +22,18 @@ def _stream_handle(stream=None) -> int:
     return int(s.cuda_stream)
 
 
+def _to_device(arr: np.ndarray, device) -> torch.Tensor:
+    """Device copy of a host array that may be read-only (a SparseCooTensor's arrays are,
+    sparse.py:101-107): the host tensor is only ever the source of the copy, so torch's
+    non-writable warning does not apply."""
+    if not arr.flags.writeable:
+        import warnings
+        with warnings.catch_warnings():
+            warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+            return torch.from_numpy(arr).to(device)
+    return torch.from_numpy(arr).to(device)
+
+
 class DeviceCoo:
     """A d-way COO tensor resident on one GPU, SoA columns + values."""
 
@@ -51,8 +63,8 @@ class DeviceCoo:
     @classmethod
     def from_host(cls, subs, vals, shape, device="cuda"):
         subs = np.asarray(subs, dtype=np.int64).reshape(-1, len(shape))
-        cols = [torch.from_numpy(np.ascontiguousarray(subs[:, m])).to(device) for m in range(len(shape))]
-        v = torch.from_numpy(np.ascontiguousarray(np.asarray(vals, dtype=np.float64))).to(device)
+        cols = [_to_device(np.ascontiguousarray(subs[:, m]), device) for m in range(len(shape))]
+        v = _to_device(np.ascontiguousarray(np.asarray(vals, dtype=np.float64)), device)
         return cls(cols, v, shape)
 
     @classmethod

@@ -382,6 +382,26 @@ def test_host_pipeline_declines_unsorted_and_reports_index_errors():
         _host_ttv(bad, vals, shape, x.cpu().numpy(), 2)
 
 
+def test_host_pipeline_pinned_and_unpackable_chunks(oracle):
+    """The pipelined host call with (a) pinned caller buffers (direct DMA, no staging) and
+    (b) pageable buffers whose first chunk holds a negative kept index (no packed form: that chunk
+    travels as raw int64 rows) -- both bit-exact against the oracle."""
+    import torch
+    shape = (300000, 2000, 3000)
+    subs, vals = oracle.gen_coo(shape, 20_000_000, zipf_s=1.1, normal_vals=True, seed=31)
+    x = oracle.gen_uniform(shape[2], 8)
+    es, ev, _ = oracle.ttv_raw(subs, vals, shape, x, 2)
+    ps = torch.from_numpy(subs).pin_memory()
+    pv = torch.from_numpy(vals).pin_memory()
+    s, v = _host_ttv(ps.numpy(), pv.numpy(), shape, x, 2)
+    assert s.tobytes() == es.tobytes() and v.tobytes() == ev.tobytes()
+    g = subs.copy()
+    g[0, 0] = -7  # still lexicographically first: garbage kept index, canonical order kept
+    es2, ev2, _ = oracle.ttv_raw(g, vals, shape, x, 2)
+    s2, v2 = _host_ttv(g, vals, shape, x, 2)
+    assert s2.tobytes() == es2.tobytes() and v2.tobytes() == ev2.tobytes()
+
+
 def _canonical_coo(shape, nnz, seed):
     """Distinct uniform coordinates in canonical (lexicographic) order, positive values."""
     rng = np.random.default_rng(seed)
@@ -769,3 +789,40 @@ def test_c_abi_timed_and_one_process_multi_device(oracle):
     cat_s = torch.cat([outs[i][0][:counts[i]] for i in range(3)])
     cat_v = torch.cat([outs[i][1][:counts[i]] for i in range(3)])
     assert torch.equal(cat_s, s0[:u0]) and torch.equal(cat_v, v0[:u0])
+
+
+def test_cfg5_shape_1e8_rows_against_reference(oracle):
+    """Full-scale parity: 1e8 rows of the config-5 shape (Zipf 1.2, N(0,1)
+    values), the device TTV and the drop-in host call (pageable arrays, packed staging) against the
+    reference's own kernel (oracle/_ref, key-aligned shards on every host thread) -- bit-exact."""
+    import paper_2510_01495_b200 as tk
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (10**6, 10**5, 10**4)
+    t = DeviceCoo.generate(shape, 100_000_000, zipf_s=1.2, normal_vals=True, seed=12345)
+    x = uniform_vector(shape[2], 777)
+    u, os_d, ov_d = t.ttv(x, 2)
+    gs, gv = os_d[:u].cpu().numpy(), ov_d[:u].cpu().numpy()
+    subs, vals = t.to_host()
+    del t, os_d, ov_d
+    xh = x.cpu().numpy()
+    parts, _, kind = oracle.ttv_raw_threads(subs, vals, shape, xh, 2)
+    assert oracle.compare_parts(parts, gs, gv), kind
+    hs, hv, hsh = tk.kernels().ttv_raw(subs, vals, shape, xh, 2)
+    assert hsh == (shape[0], shape[1])
+    assert oracle.compare_parts(parts, hs, hv)
+
+
+def test_cfg4_shape_1e8_rows_against_chained_reference(oracle):
+    """Config 4 at full size: the fused dense TTV within 1e-12 relative of the chain of the
+    reference's ttv_raw (modes 3, 2, 1), densified -- SURVEY 8c's config-4 oracle."""
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (20000,) * 4
+    t = DeviceCoo.generate(shape, 100_000_000, seed=4444)
+    vecs = {m: uniform_vector(shape[m], 40 + m) for m in (1, 2, 3)}
+    got = t.ttv_dense(vecs, 0).cpu().numpy()
+    subs, vals = t.to_host()
+    del t
+    ref, _, _ = oracle.ttv_multi_dense_threads(subs, vals, shape, {m: v.cpu().numpy() for m, v in vecs.items()}, 0)
+    nz = ref != 0
+    assert np.array_equal(got[~nz], ref[~nz])
+    assert np.max(np.abs(got[nz] - ref[nz]) / np.abs(ref[nz])) <= 1e-12

@@ -70,7 +70,7 @@ def test_b200_label_matches_native_loop(ref, experiment, size, extra):
         got = _thunk_out(ref, label, cfg, size)
         exp = _thunk_out(ref, "native-loop", cfg, size)
         if experiment == "ttv":
-            gs, gv = (got.subs, got.vals) if hasattr(got, "subs") else (got[0], got[1])
+            gs, gv = (got.subs, got.vals) if hasattr(got, "subs") else (got[0], got[1])  # HostSparseTensor
             es, ev = exp[0], exp[1]
             assert np.asarray(gs).tobytes() == np.asarray(es).tobytes(), label
             assert np.asarray(gv).tobytes() == np.asarray(ev).tobytes(), label
@@ -94,8 +94,8 @@ def test_bound_kernel_set_with_b200_module(ref):
     t = ref.gen_sparse3(ref.GenSpec(9, "sparse3", (80, 70, 60), 0.02))
     v = r.random(70)
     got, exp = ours.ttv(t.subs, t.vals, t.shape, v, 1), theirs.ttv(t.subs, t.vals, t.shape, v, 1)
-    assert got.subs.tobytes() == exp.subs.tobytes() and got.vals.tobytes() == exp.vals.tobytes()
-    assert got.shape == exp.shape
+    assert got.new_subs.tobytes() == exp.new_subs.tobytes() and got.new_vals.tobytes() == exp.new_vals.tobytes()
+    assert got.new_shape == exp.new_shape
 
 
 @pytest.mark.gpu
