@@ -30,11 +30,8 @@ struct Counters {
   unsigned long long groups;     // number of output groups (before zero elimination)
   unsigned long long zeros;      // groups whose serial sum is exactly 0.0
   unsigned int flags;            // kFlag* bits
-  unsigned int tile_ticket;      // dynamic tile ids (in launch order) for look-back
-  unsigned long long q_head;     // chain-job queue: next ticket handed to a chain warp
-  unsigned long long q_tail;     // chain-job queue: jobs pushed so far
-  unsigned int streamers_done;   // CTAs whose streamer warps have finished
-  unsigned int grab_ticket;      // stream kernel: tiles handed to CTAs in processing order
+  unsigned int tile_ticket;      // watchdog report: the tile whose wait gave up
+  unsigned int grab_ticket;      // watchdog report: the wait site that gave up
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -63,22 +60,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-// bytes must be a multiple of 16, both addresses 16-byte aligned.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
 // ---- relaxed GPU-scope accesses for the look-back status words ------------------------------
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
@@ -87,12 +68,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 }
 __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Streaming 8-byte loads that should not displace reusable lines.
-template <class T>
-__device__ __forceinline__ T ld_stream(const T* p) {
-  return __ldcs(p);
 }
 
 // ---- per-tile status words of the tile kernel's prefix scan -------------------------------------

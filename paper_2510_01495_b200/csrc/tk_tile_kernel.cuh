@@ -212,17 +212,21 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   __shared__ int s_known, s_last, s_consumed;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long ntiles = (p.n + TILE - 1) / TILE;
-  if (blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
+  const long long ntiles = p.ntiles;
+  if (p.mode == kTileSinglePass && blockIdx.x == 0) {  // dispatched first, stays resident: the prefix scanner
     if (warp == 0) tile_scanner<TK_SCAN_D>(p.status, ntiles, p.ctr);
     return;
   }
-  // Blocks are dispatched in index order (the single-pass scan convention).  Block b COUNTS the
-  // heads of tile b-1 (publishing its aggregate) and FOLDS tile b-1-lag: the prefix of a tile is
-  // therefore published ~lag tiles before anyone needs it, and the fold's key columns are
-  // L2-hot from the count.
-  const long long count_tile = (long long)blockIdx.x - 1;
-  const long long fold_tile = count_tile - p.lag;
+  // Single pass: blocks are dispatched in index order (the single-pass scan convention; if that
+  // ever fails, e.g. under MPS or SM partitioning, a wait gives up and the host re-runs the call
+  // as three order-independent passes: kTileCountOnly, scan_tile_status, kTileFoldOnly).  Block b
+  // COUNTS the heads of tile b-1 (publishing its aggregate) and FOLDS tile b-1-lag: the prefix of
+  // a tile is therefore published ~lag tiles before anyone needs it, and the fold's key columns
+  // are L2-hot from the count.
+  const long long count_tile = p.mode == kTileSinglePass ? (long long)blockIdx.x - 1
+                               : p.mode == kTileCountOnly ? (long long)blockIdx.x : -1;
+  const long long fold_tile = p.mode == kTileSinglePass ? count_tile - p.lag
+                              : p.mode == kTileFoldOnly ? (long long)blockIdx.x : -1;
   TKR_START();
   // the fold tile's status word, read now: published ~lag tiles ago, so this is almost always the
   // prefix already and its L2 round trip overlaps the count instead of delaying the fold
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // ---- L2 prefetch: the key columns of tile count_tile + TK_TILE_PF (the count's loads, and ~lag
   //      tiles later the fold's copy, then hit L2) and the value columns of tile fold_tile +
   //      TK_TILE_PFV (close to their use, so they do not crowd L2); HBM sees these async requests ----
-  if (TK_TILE_PF > 0 && warp == 1 && lane < ncol) {
+  if (TK_TILE_PF > 0 && p.mode == kTileSinglePass && warp == 1 && lane < ncol) {
     const long long pt = lane < nk ? count_tile + TK_TILE_PF : fold_tile + TK_TILE_PFV;
     if (pt >= 0 && pt < ntiles) {
       const long long ps = pt * TILE;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
   // Each warp takes 128 consecutive rows; the previous row's key comes from the neighbouring lane
   // (lane 31 carries the row before the warp's first row, then the previous iteration's last row).
   // The order check (kept keys non-decreasing) lives here too, while the keys are in registers.
-  if (count_tile < ntiles) {
+  if (count_tile >= 0 && count_tile < ntiles) {
     const long long cstart = count_tile * TILE;
     const int ccnt = (int)min((long long)TILE, p.n - cstart);
     const int wrow0 = warp * (TILE / kTileWarps);
@@ -717,6 +721,29 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
       if (NK > 0 || c < nk) k[c] = gk[c];
     seg_emit<SRC>(p, base + open_li, k, acc);
     TKR(7);
+  }
+}
+
+// Order-independent prefix for the three-pass fallback: status[t] holds tile t's complete
+// aggregate (kTileCountOnly); one CTA turns the words into inclusive prefixes (kStPre | prefix).
+__global__ void __launch_bounds__(1024) scan_tile_status_kernel(unsigned long long* status, long long ntiles) {
+  __shared__ unsigned long long s_sum[1024];
+  const long long per = (ntiles + 1023) / 1024;
+  const long long a = min(ntiles, (long long)threadIdx.x * per), b = min(ntiles, a + per);
+  unsigned long long run = 0;
+  for (long long t = a; t < b; ++t) run += status[t] & kStCntMask;
+  s_sum[threadIdx.x] = run;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned long long v = threadIdx.x >= (unsigned)o ? s_sum[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    s_sum[threadIdx.x] += v;
+    __syncthreads();
+  }
+  run = s_sum[threadIdx.x] - run;  // exclusive prefix of this thread's range
+  for (long long t = a; t < b; ++t) {
+    run += status[t] & kStCntMask;
+    status[t] = kStPre | run;
   }
 }
 

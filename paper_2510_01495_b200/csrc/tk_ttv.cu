@@ -696,20 +696,44 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
     p.prof = prof.as<unsigned long long>();
   }
 #endif
-  ktimer_begin(st);
-  // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
   p.lag = std::min<long long>(TK_TILE_LAG, ntiles);
+  p.ntiles = ntiles;
   p.out_v2 = p.out_nk == 2 && aligned16(p.out_subs);
-  kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
-  ktimer_end(st);
-  count_launch();
-  TK_CUDA(cudaGetLastError());
-  TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaStreamSynchronize(st));
-  if (host_ctr->flags & kFlagStall)
-    return fail(TK_ECUDA, "internal error: tile pipeline wait gave up (site " +
-                              std::to_string(host_ctr->grab_ticket) + ", tile " +
-                              std::to_string(host_ctr->tile_ticket) + ")");
+  const char* mp = getenv("TK_TILE_MULTIPASS");  // tests force the fallback with "1"
+  bool stalled = mp && mp[0] == '1';
+  if (!stalled) {
+    // block 0: the prefix scanner; block b counts tile b-1 and folds tile b-1-lag
+    ktimer_begin(st);
+    p.mode = kTileSinglePass;
+    kern<<<(unsigned)(ntiles + p.lag + 1), kTileThreads, smem, st>>>(p);
+    ktimer_end(st);
+    count_launch();
+    TK_CUDA(cudaGetLastError());
+    TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    stalled = (host_ctr->flags & kFlagStall) != 0;
+  }
+  if (stalled) {
+    // The single pass relies on in-order block dispatch; a wait gave up (or the fallback was
+    // forced): redo the call as three order-independent launches.  Every tile's output lands at
+    // the same place, so rows the stalled pass already wrote are simply rewritten.
+    TK_CUDA(cudaMemsetAsync(b, 0, status_b + 256, st));
+    ktimer_begin(st);
+    p.mode = kTileCountOnly;
+    kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(p);
+    scan_tile_status_kernel<<<1, 1024, 0, st>>>(p.status, ntiles);
+    p.mode = kTileFoldOnly;
+    kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(p);
+    ktimer_end(st);
+    count_launch(3);
+    TK_CUDA(cudaGetLastError());
+    TK_CUDA(cudaMemcpyAsync(host_ctr, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    if (host_ctr->flags & kFlagStall)
+      return fail(TK_ECUDA, "internal error: tile pipeline wait gave up (site " +
+                                std::to_string(host_ctr->grab_ticket) + ", tile " +
+                                std::to_string(host_ctr->tile_ticket) + ")");
+  }
 #ifdef TK_TRACE
   if (trace_file) {
     std::vector<unsigned long long> h((size_t)nblk * 8);

@@ -24,6 +24,12 @@ enum SrcKind : int {
   kSrcLinKey = 2,  // one linearised kept key (sorted) + precomputed w; decode on output
 };
 
+enum TileMode : int {
+  kTileSinglePass = 0,  // lagged count/fold with the scanner block (needs in-order block dispatch)
+  kTileCountOnly = 1,   // fallback pass 1: block t counts tile t
+  kTileFoldOnly = 2,    // fallback pass 3: block t folds tile t (prefixes already scanned)
+};
+
 struct SegParams {
   long long n;                       // rows in the stream
   int nk;                            // key columns in the stream (kSrcLinKey: 1)
@@ -43,6 +49,8 @@ struct SegParams {
   int bulk_ok;                       // all stream pointers 16-byte aligned
   unsigned long long* prof;          // optional phase counters (TK_TILE_PROFILE=1), else null
   long long lag;                     // tile kernel: block b counts tile b-1 and folds tile b-1-lag
+  long long ntiles;                  // tile kernel: ceil(n / TILE), computed on the host
+  int mode;                          // tile kernel: TileMode
   int out_v2;                        // out_nk == 2 and out_subs 16-byte aligned: one 16-byte key store
 };
 
@@ -103,13 +111,6 @@ __device__ __forceinline__ void seg_emit(const SegParams& p, long long g, const 
 
 
 // ---- general path helpers --------------------------------------------------------------------
-
-// w = vals * x[subk] and the linearised kept key (row-major over kept modes == lexicographic
-// order when every kept index is in bounds).  Flags contracted-mode and kept-mode range errors.
-__global__ void prep_linkey_kernel(long long n, int nk, const long long* const* __restrict__ keep_cols_ptr,
-                                   const long long* __restrict__ subk, const double* __restrict__ vals,
-                                   const double* __restrict__ x, long long nx, const long long* __restrict__ dims,
-                                   long long* __restrict__ key, double* __restrict__ w, Counters* ctr);
 
 __global__ void iota_kernel(long long n, long long* out);
 __global__ void gather_i64_kernel(long long n, const long long* __restrict__ src, const long long* __restrict__ idx,

@@ -826,3 +826,28 @@ def test_cfg4_shape_1e8_rows_against_chained_reference(oracle):
     nz = ref != 0
     assert np.array_equal(got[~nz], ref[~nz])
     assert np.max(np.abs(got[nz] - ref[nz]) / np.abs(ref[nz])) <= 1e-12
+
+
+def test_tile_three_pass_fallback_bit_exact(oracle, monkeypatch, golden_small, golden_hashes):
+    """The order-independent fallback of the single-pass tile kernel (count pass, one-CTA scan,
+    fold pass -- what a call re-runs if in-order block dispatch ever fails and a wait gives up),
+    forced with TK_TILE_MULTIPASS=1: bit-exact on the golden cases and on a Zipf tensor with
+    groups spanning many tiles, sorted-stream and sort paths."""
+    import paper_2510_01495_b200 as tk
+    monkeypatch.setenv("TK_TILE_MULTIPASS", "1")
+    K = tk.kernels()
+    n = 0
+    for name, subs, vals, shape, x, k, err, exp in ttv_cases(golden_small, golden_hashes):
+        if err:
+            continue
+        s, v, sh = K.ttv_raw(subs, vals, shape, x, k)
+        assert s.tobytes() == exp[0].tobytes() and v.tobytes() == exp[1].tobytes(), name
+        n += 1
+    assert n >= 100
+    shape = (2000, 300, 400)
+    subs, vals = oracle.gen_coo(shape, 3_000_000, zipf_s=1.3, normal_vals=True, seed=8)
+    for k in (2, 1, 0):
+        x = oracle.gen_uniform(shape[k], 3 + k)
+        es, ev, _ = oracle.ttv_raw(subs, vals, shape, x, k)
+        s, v, _ = K.ttv_raw(subs, vals, shape, x, k)
+        assert s.tobytes() == es.tobytes() and v.tobytes() == ev.tobytes(), k
