@@ -177,21 +177,29 @@ def barrier(world):
         dist.barrier()
 
 
-def coll_device():
-    """Where collective operands live: the GPU under NCCL, the host under gloo."""
-    import torch
+def make_comm(rank, world):
+    """The data-plane communicator: NCCL inside libtk_b200.so (multi.NcclComm; torch.distributed
+    only broadcasts its id).  The one-GPU path check (TK_BENCH_BACKEND=gloo) uses the gloo
+    stand-in of the tests instead -- NCCL cannot put two ranks on one GPU."""
+    if world == 1:
+        return None
     import torch.distributed as dist
-    return torch.device("cuda") if dist.get_backend() == "nccl" else torch.device("cpu")
+    if dist.get_backend() != "nccl":
+        sys.path.insert(0, os.path.join(REPO, "tests"))
+        from gloo_comm import GlooComm
+        return GlooComm()
+    from paper_2510_01495_b200 import multi
+    return multi.NcclComm(rank, world)
 
 
 def max_over_ranks(v: float, world: int) -> float:
+    """Max of a host scalar over ranks (harness bookkeeping after the timed region)."""
     if world == 1:
         return v
-    import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=coll_device())
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    box = [None] * world
+    dist.all_gather_object(box, float(v))
+    return max(box)
 
 
 def cpu_info():
@@ -445,7 +453,7 @@ def secondary_measurements(rank, steps, threads, with_cpu):
     return res
 
 
-def multi_dense_measurement(rank, world, steps, warmup):
+def multi_dense_measurement(rank, world, steps, warmup, comm):
     """Config 4 sharded across the ranks: the kernel-store merge
     (multi.PeerDenseMerge: every shard's dense-TTV kernel stores its owned keep-mode range into
     all ranks' NVLink-mapped output vectors, then a one-element barrier) against the NCCL
@@ -464,7 +472,7 @@ def multi_dense_measurement(rank, world, steps, warmup):
     t = full.slice(bounds[rank], bounds[rank + 1]) if world > 1 else full
     del full
     torch.cuda.empty_cache()
-    merge = multi.PeerDenseMerge(shape[0], torch.cuda.current_device())
+    merge = multi.PeerDenseMerge(shape[0], torch.cuda.current_device(), comm)
     red = torch.empty(shape[0], dtype=torch.float64, device="cuda")
 
     def peer_step():
@@ -472,10 +480,7 @@ def multi_dense_measurement(rank, world, steps, warmup):
 
     def nccl_step():
         t.ttv_dense(vecs, 0, red)
-        if dist.get_backend() == "nccl":
-            multi.merge_dense(red)
-        else:  # path check under gloo: the same sum through the host
-            red.copy_(multi.merge_dense(red.cpu()))
+        multi.merge_dense(comm, red)
 
     res = {}
     for name, fn in (("kernel_store_merge", peer_step), ("nccl_allreduce_merge", nccl_step)):
@@ -527,13 +532,14 @@ def run_ours(args):
     out_vals = torch.empty(max(n_local, 1), dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
 
+    comm = make_comm(rank, world)
     pending = [None]  # N > 1: the previous step's count all-gather, finished while this step's kernel runs
 
     def step():
         u, _, _ = t.ttv(x, k, out_subs, out_vals)
         if world > 1:
-            h = multi.gather_counts_async(u, coll_device())
-            counts = multi.wait_counts(pending[0]) if pending[0] is not None else None
+            h = comm.counts_start(u, stream)  # NCCL all-gather on the comm's stream, after the TTV
+            counts = comm.counts_wait(pending[0]) if pending[0] is not None else None
             pending[0] = h
             return u, counts
         return u, [u]
@@ -541,7 +547,7 @@ def run_ours(args):
     def drain():  # the last step's offsets (inside the timed region)
         if pending[0] is None:
             return None
-        c = multi.wait_counts(pending[0])
+        c = comm.counts_wait(pending[0])
         pending[0] = None
         return c
 
@@ -625,7 +631,7 @@ def run_ours(args):
     if world > 1 and not args.no_secondary:
         del out_subs, out_vals, t
         torch.cuda.empty_cache()
-        multi_dense = multi_dense_measurement(rank, world, max(3, min(args.steps, 10)), 3)
+        multi_dense = multi_dense_measurement(rank, world, max(3, min(args.steps, 10)), 3, comm)
 
     if rank == 0:
         line = {
@@ -654,6 +660,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
+        comm.close()
         dist.destroy_process_group()
     return 0
 

@@ -40,6 +40,7 @@ typedef enum tk_status {
   TK_EORDER = 3,   /* tenkern.OrderError      (d < 2)                                  */
   TK_EINDEX = 4,   /* tenkern.DimensionError  (mode-k index outside x, pyx:361-365)    */
   TK_ECUDA = 6,    /* CUDA runtime failure                                             */
+  TK_ENCCL = 7,    /* NCCL failure (library missing, communicator or collective error) */
   TK_EARG = 8,     /* unsupported argument (e.g. order > TK_MAX_ORDER, null pointer)   */
   TK_ENOMEM = 9    /* device allocation failed                                         */
 } tk_status;
@@ -202,6 +203,33 @@ int tk_multi_ttv_f64(int32_t d, const int64_t* shape, int32_t k, int32_t nshard,
                      int64_t* const* shard_out_subs, double* const* shard_out_vals, int64_t* shard_out_nnz,
                      int64_t* out_offsets);
 int tk_multi_free(void);
+
+/* ---- multi-GPU data plane: NCCL inside the library ------------------------
+ * One process per GPU.  The reference has no distributed code; this is the
+ * exchange the sharded TTV needs: per-rank result counts (offsets), the optional gather of the
+ * sparse slices to a root, the IPC-handle exchange and stream-ordered barrier of the dense
+ * peer-store merge, and the all-reduce merge baseline.  NCCL is bound at run time (dlopen; the
+ * copy already in the process -- PyTorch's -- is reused, or the path given to tk_nccl_load).
+ * Bootstrap: rank 0 calls tk_nccl_get_unique_id and ships the 128 bytes to the other ranks by
+ * any means (torch.distributed broadcast); every rank then calls tk_nccl_comm_init on its
+ * current device.  Collectives are enqueued on the caller's stream unless noted. */
+int tk_nccl_load(const char* path);
+int tk_nccl_version(int* version);
+int tk_nccl_get_unique_id(void* id128);
+int tk_nccl_comm_init(const void* id128, int32_t nranks, int32_t rank, void** comm);
+int tk_nccl_comm_free(void* comm);
+int tk_nccl_rank(void* comm, int32_t* rank, int32_t* nranks);
+/* all-gather of one host count per rank, after `stream`, on the comm's own stream (non-blocking);
+ * tk_nccl_counts_wait returns the counts (rank order) of a ticket */
+int tk_nccl_counts_start(void* comm, int64_t count, void* stream, int32_t* ticket);
+int tk_nccl_counts_wait(void* comm, int32_t ticket, int64_t* counts);
+/* the ranks' (counts[r], nk) row-major slices gathered to `root` in rank order (device buffers) */
+int tk_nccl_gather_rows(void* comm, int32_t root, const int64_t* subs, const double* vals, int32_t nk,
+                        const int64_t* counts, int64_t* dst_subs, double* dst_vals, void* stream);
+/* every rank's nbytes of host data to every rank (host buffers; synchronous) */
+int tk_nccl_allgather_bytes(void* comm, const void* host_src, void* host_dst, int64_t nbytes);
+int tk_nccl_barrier(void* comm, void* stream);
+int tk_nccl_allreduce_sum_f64(void* comm, double* buf, int64_t n, void* stream);
 
 /* ---- timing helper ----------------------------------------------------------------------- */
 /* Device milliseconds between two points on a stream (cudaEvent pair). */

@@ -15,7 +15,7 @@ from . import errors
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtk_b200.so")
 
-TK_OK, TK_EDIM, TK_EMODE, TK_EORDER, TK_EINDEX, TK_ECUDA, TK_EARG, TK_ENOMEM = 0, 1, 2, 3, 4, 6, 8, 9
+TK_OK, TK_EDIM, TK_EMODE, TK_EORDER, TK_EINDEX, TK_ECUDA, TK_ENCCL, TK_EARG, TK_ENOMEM = 0, 1, 2, 3, 4, 6, 7, 8, 9
 MAX_ORDER = 16
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -66,6 +66,18 @@ SIGNATURES = {
     "tk_multi_ttv_f64": (ctypes.c_int, [ctypes.c_int32, _c_i64p, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp,
                                         _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
     "tk_multi_free": (ctypes.c_int, []),
+    "tk_nccl_load": (ctypes.c_int, [ctypes.c_char_p]),
+    "tk_nccl_version": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "tk_nccl_get_unique_id": (ctypes.c_int, [_vp]),
+    "tk_nccl_comm_init": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "tk_nccl_comm_free": (ctypes.c_int, [_vp]),
+    "tk_nccl_rank": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "tk_nccl_counts_start": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.POINTER(ctypes.c_int32)]),
+    "tk_nccl_counts_wait": (ctypes.c_int, [_vp, ctypes.c_int32, _c_i64p]),
+    "tk_nccl_gather_rows": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, ctypes.c_int32, _c_i64p, _vp, _vp, _vp]),
+    "tk_nccl_allgather_bytes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
+    "tk_nccl_barrier": (ctypes.c_int, [_vp, _vp]),
+    "tk_nccl_allreduce_sum_f64": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
     "tk_timer_start": (ctypes.c_int, [_vp]),
     "tk_timer_stop": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "tk_release": (ctypes.c_int, []),
@@ -100,6 +112,7 @@ _STATUS_EXC = {
     TK_EORDER: errors.OrderError,
     TK_EARG: errors.ConfigError,
     TK_ECUDA: errors.DeviceError,
+    TK_ENCCL: errors.DeviceError,
     TK_ENOMEM: errors.DeviceError,
 }
 

@@ -700,19 +700,24 @@ int tk_multi_ttv_f64(int32_t d, const int64_t* shape, int32_t k, int32_t nshard,
   }
   std::vector<int> rcs(nshard, TK_OK);
   std::vector<std::string> errs(nshard);
-  std::vector<std::thread> th;
-  for (int s = 0; s < nshard; ++s)
-    th.emplace_back([&, s] {
-      if (cudaSetDevice(shard_device[s]) != cudaSuccess) {
-        rcs[s] = TK_ECUDA;
-        errs[s] = "cudaSetDevice failed";
-        return;
-      }
-      rcs[s] = tk_ttv_f64_device(d, shape, shard_nnz[s], shard_cols[s], nullptr, shard_vals[s], shard_x[s], nx, k,
-                                 shard_out_subs[s], shard_out_vals[s], &shard_out_nnz[s], st[s]);
-      if (rcs[s]) errs[s] = tk_last_error();
-    });
-  for (auto& t : th) t.join();
+  int caller_dev = 0;
+  TK_CUDA(cudaGetDevice(&caller_dev));
+  // one shard per worker of the persistent host pool (no per-call threads: the workers' cached
+  // pinned scratch and timing events are reused across calls)
+  parallel_for(nshard, [&](int s) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(shard_device[s]) != cudaSuccess) {
+      rcs[s] = TK_ECUDA;
+      errs[s] = "cudaSetDevice failed";
+      return;
+    }
+    rcs[s] = tk_ttv_f64_device(d, shape, shard_nnz[s], shard_cols[s], nullptr, shard_vals[s], shard_x[s], nx, k,
+                               shard_out_subs[s], shard_out_vals[s], &shard_out_nnz[s], st[s]);
+    if (rcs[s]) errs[s] = tk_last_error();
+    cudaSetDevice(prev);
+  });
+  TK_CUDA(cudaSetDevice(caller_dev));
   for (int s = 0; s < nshard; ++s)
     if (rcs[s]) return fail(rcs[s], errs[s]);  // the error message is thread-local: carry it over
   out_offsets[0] = 0;

@@ -38,7 +38,7 @@ class HostPool {
   int size() const { return size_; }
   // fn(i) for i in [0, n) on the workers and the caller; returns when every part is done
   void run(int n, const std::function<void(int)>& fn) {
-    if (n <= 1 || size_ == 1) {
+    if (n <= 1 || size_ == 1 || in_job_) {  // nested use from inside a job runs inline
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
@@ -63,7 +63,9 @@ class HostPool {
     for (;;) {
       const int i = next_.fetch_add(1);
       if (i >= n_) return;
+      in_job_ = true;
       (*job_)(i);
+      in_job_ = false;
       std::lock_guard<std::mutex> lk(mu_);
       if (--pending_ == 0) done_.notify_all();
     }
@@ -79,6 +81,7 @@ class HostPool {
       work();
     }
   }
+  static thread_local bool in_job_;
   std::vector<std::thread> th_;
   std::mutex mu_, run_mu_;
   std::condition_variable cv_, done_;
@@ -87,6 +90,8 @@ class HostPool {
   std::atomic<int> next_{0};
   uint64_t gen_ = 0;
 };
+
+thread_local bool HostPool::in_job_ = false;
 
 HostPool& pool() {
   static HostPool* p = new HostPool();  // never destroyed: workers may outlive static teardown

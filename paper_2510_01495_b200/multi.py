@@ -1,4 +1,5 @@
-"""Sharding of the TTV path across GPUs (one process per GPU, torch.distributed plumbing).
+"""Sharding of the TTV path across GPUs (one process per GPU; the data plane is NCCL inside
+libtk_b200.so, torch.distributed only bootstraps the communicator).
 
 Nonzeros are independent units; the only exchange is the merge of results:
 
@@ -6,24 +7,30 @@ Nonzeros are independent units; the only exchange is the merge of results (SURVE
   to the next change of the kept-mode key, so no output group spans two ranks;
 * sparse result (configs 3, 5): every rank's output is a canonical slice and the
   rank-order concatenation IS the canonical result, bitwise equal to one GPU; the merge is
-  an all-gather of per-rank counts (global offsets), no data moves;
+  an all-gather of per-rank counts (global offsets, ``NcclComm.counts_start``), no data
+  moves; ``gather_sparse_to_root`` optionally collects the slices on one rank;
 * dense result (config 4): each rank owns the keep-mode indices of its shard.  The B200
   path (``PeerDenseMerge``) has the TTV kernel itself store every owned element -- values,
   and zeros for indices without rows -- into every rank's output vector, mapped over NVLink
-  by CUDA IPC, so one stream-ordered barrier completes the merge (no all-reduce of the
-  vector).  ``merge_dense`` keeps the all-reduce form (each rank writes only its rows into a
-  zeroed full-length vector; every element has exactly one non-zero contributor, so the sum
-  is exact) as the NCCL baseline.
+  by CUDA IPC (handles exchanged once through the communicator), so one stream-ordered
+  barrier completes the merge (no all-reduce of the vector).  ``merge_dense`` keeps the
+  all-reduce form (each rank writes only its rows into a zeroed full-length vector; every
+  element has exactly one non-zero contributor, so the sum is exact) as the NCCL baseline.
 
-The host-side logic here is exercised with gloo on CPU (tests/test_multi_cpu.py); on the
-GPU box the same calls run over NCCL.
+Every function that exchanges data takes a communicator with the ``NcclComm`` interface.  The
+host-side logic is exercised on CPU with a gloo-backed stand-in (tests/gloo_comm.py); on a GPU
+node ``NcclComm`` runs it over NVLink.
 """
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 import torch
-import torch.distributed as dist
+
+from . import _lib
 
 
 def kept_prefix_key(cols, nkeep: int, dims) -> torch.Tensor:
@@ -67,30 +74,6 @@ def shard_bounds_np(key: np.ndarray, world: int) -> list:
     return bounds
 
 
-def gather_counts(u: int, device) -> list:
-    """All-gather per-rank output counts; returns the list in rank order."""
-    world = dist.get_world_size()
-    t = torch.tensor([u], dtype=torch.int64, device=device)
-    out = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
-    return [int(v.item()) for v in out]
-
-
-def gather_counts_async(u: int, device):
-    """Start the all-gather of per-rank output counts without waiting for it (the next step's
-    TTV kernel runs while it completes); finish with ``wait_counts``."""
-    world = dist.get_world_size()
-    t = torch.tensor([u], dtype=torch.int64, device=device)
-    out = [torch.zeros_like(t) for _ in range(world)]
-    return dist.all_gather(out, t, async_op=True), out
-
-
-def wait_counts(handle) -> list:
-    work, out = handle
-    work.wait()
-    return [int(v.item()) for v in out]
-
-
 def global_offsets(counts) -> list:
     off = [0]
     for c in counts:
@@ -116,26 +99,139 @@ def owned_key_range(key: torch.Tensor, bounds, rank: int, nkeep: int) -> tuple:
     return lo, max(lo, hi)
 
 
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _torch_nccl_path():
+    """PyTorch's own libnccl (so the process holds one NCCL), if it ships one."""
+    try:
+        import nvidia.nccl
+        for p in nvidia.nccl.__path__:
+            f = os.path.join(p, "lib", "libnccl.so.2")
+            if os.path.exists(f):
+                return f
+    except ImportError:
+        pass
+    return None
+
+
+class NcclComm:
+    """One rank's NCCL communicator inside libtk_b200.so (tk_nccl_*, include/tk_b200.h).
+
+    ``bootstrap`` ships rank 0's 128-byte unique id to every rank; by default it is a
+    torch.distributed ``broadcast_object_list`` (the only use of torch.distributed here)."""
+
+    def __init__(self, rank: int, world: int, bootstrap=None):
+        self.lib = _lib.load()
+        path = _torch_nccl_path()
+        _lib.check(self.lib.tk_nccl_load(path.encode() if path else None))
+        self.rank, self.world = int(rank), int(world)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(self.lib.tk_nccl_get_unique_id(uid))
+        if bootstrap is None:
+            bootstrap = _torch_bootstrap
+        raw = bootstrap(uid.raw if self.rank == 0 else None)
+        uid = ctypes.create_string_buffer(bytes(raw), 128)
+        self._comm = ctypes.c_void_p()
+        _lib.check(self.lib.tk_nccl_comm_init(uid, self.world, self.rank, ctypes.byref(self._comm)))
+
+    # (a) offsets of the sparse result
+    def counts_start(self, count: int, stream=None) -> int:
+        t = ctypes.c_int32(0)
+        _lib.check(self.lib.tk_nccl_counts_start(self._comm, int(count), _stream(stream), ctypes.byref(t)))
+        return t.value
+
+    def counts_wait(self, ticket: int) -> list:
+        out = (ctypes.c_int64 * self.world)()
+        _lib.check(self.lib.tk_nccl_counts_wait(self._comm, int(ticket), out))
+        return [int(v) for v in out]
+
+    def allgather_counts(self, count: int, stream=None) -> list:
+        return self.counts_wait(self.counts_start(count, stream))
+
+    # (b) the sparse slices on one rank
+    def gather_rows(self, subs: torch.Tensor, vals: torch.Tensor, counts, root: int = 0, stream=None):
+        nk = subs.shape[1] if subs.dim() == 2 else 1
+        cnt = _lib.i64_array(counts)
+        dst_s = dst_v = None
+        if self.rank == root:
+            total = sum(counts)
+            dst_s = torch.empty((max(total, 1), nk), dtype=torch.int64, device=subs.device)
+            dst_v = torch.empty(max(total, 1), dtype=torch.float64, device=vals.device)
+        _lib.check(self.lib.tk_nccl_gather_rows(
+            self._comm, int(root), subs.data_ptr(), vals.data_ptr(), nk, cnt,
+            dst_s.data_ptr() if dst_s is not None else None, dst_v.data_ptr() if dst_v is not None else None,
+            _stream(stream)))
+        if dst_s is None:
+            return None, None
+        total = sum(counts)
+        return dst_s[:total], dst_v[:total]
+
+    # (c) dense merge: IPC handles, barrier, all-reduce baseline
+    def allgather_bytes(self, data: bytes) -> list:
+        n = len(data)
+        dst = ctypes.create_string_buffer(n * self.world)
+        _lib.check(self.lib.tk_nccl_allgather_bytes(self._comm, ctypes.create_string_buffer(data, n), dst, n))
+        return [dst.raw[r * n:(r + 1) * n] for r in range(self.world)]
+
+    def barrier(self, stream=None) -> None:
+        _lib.check(self.lib.tk_nccl_barrier(self._comm, _stream(stream)))
+
+    def allreduce_sum_(self, t: torch.Tensor, stream=None) -> torch.Tensor:
+        _lib.check(self.lib.tk_nccl_allreduce_sum_f64(self._comm, t.data_ptr(), int(t.numel()), _stream(stream)))
+        return t
+
+    def close(self) -> None:
+        if self._comm:
+            _lib.check(self.lib.tk_nccl_comm_free(self._comm))
+            self._comm = ctypes.c_void_p()
+
+
+def _torch_bootstrap(uid):
+    import torch.distributed as dist
+    box = [uid]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+def gather_counts(comm, u: int) -> list:
+    """All-gather per-rank output counts; returns the list in rank order."""
+    return comm.allgather_counts(u)
+
+
+def gather_sparse_to_root(comm, subs: torch.Tensor, vals: torch.Tensor, counts, root: int = 0):
+    """Optional gather of the distributed sparse result to ``root`` (timed separately:
+    bounded by the root's link ingress, SURVEY.md F6).  Returns (subs, vals) on root."""
+    return comm.gather_rows(subs, vals, counts, root)
+
+
+def merge_dense(comm, out: torch.Tensor) -> torch.Tensor:
+    """Sum the per-rank dense partials in place (disjoint supports: exact)."""
+    return comm.allreduce_sum_(out)
+
+
 class PeerDenseMerge:
     """Sharded dense TTV merged by the kernel's own NVLink stores (stage 2).
 
     Every rank allocates its output vector in an exportable allocation, the 64-byte CUDA IPC
-    handles are all-gathered once, and each rank maps its peers' vectors.  ``run`` launches
-    ``tk_ttv_dense_f64_device_peers`` with all N output pointers and the rank's owned key range,
-    then a stream-ordered barrier (a one-element all-reduce: it completes only after every
-    rank's kernel, hence every peer store, has finished).  Afterwards every rank's ``out`` holds
-    the full result, identical on all ranks.
+    handles are all-gathered once through the communicator, and each rank maps its peers'
+    vectors.  ``run`` launches ``tk_ttv_dense_f64_device_peers`` with all N output pointers and
+    the rank's owned key range, then the communicator's stream-ordered barrier (it completes only
+    after every rank's kernel, hence every peer store, has finished).  Afterwards every rank's
+    ``out`` holds the full result, identical on all ranks.
     """
 
-    def __init__(self, nkeep: int, device_index: int):
+    def __init__(self, nkeep: int, device_index: int, comm):
         from .device import IpcVector, ipc_open
-        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.world
         self.local = IpcVector(nkeep, device_index)
-        handles = [None] * self.world
-        dist.all_gather_object(handles, self.local.handle())
+        handles = comm.allgather_bytes(self.local.handle())
         self.ptrs = [self.local.ptr if r == self.rank else ipc_open(h) for r, h in enumerate(handles)]
         self.device = torch.device(f"cuda:{device_index}")
-        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     @property
     def out(self) -> torch.Tensor:
@@ -143,52 +239,17 @@ class PeerDenseMerge:
 
     def run(self, dt, vecs: dict, keep: int, key_lo: int, key_hi: int, stream=None) -> torch.Tensor:
         dt.ttv_dense_peers(vecs, keep, self.ptrs, key_lo, key_hi, stream)
-        self.barrier()
+        self.comm.barrier(stream)
         return self.out
-
-    def barrier(self):
-        if dist.get_backend() == "nccl":
-            dist.all_reduce(self._flag)  # stream-ordered behind the kernel on every rank
-        else:
-            torch.cuda.synchronize(self.device)
-            dist.barrier()
 
     def close(self):
         from .device import ipc_close
         torch.cuda.synchronize(self.device)
-        dist.barrier()  # nobody stores into a mapping that is going away
+        self.comm.barrier()  # nobody stores into a mapping that is going away
+        torch.cuda.synchronize(self.device)
         for r, p in enumerate(self.ptrs):
             if r != self.rank:
                 ipc_close(p)
-        dist.barrier()
+        self.comm.barrier()
+        torch.cuda.synchronize(self.device)
         self.local.free()
-
-
-def merge_dense(out: torch.Tensor) -> torch.Tensor:
-    """Sum the per-rank dense partials in place (disjoint supports: exact)."""
-    dist.all_reduce(out, op=dist.ReduceOp.SUM)
-    return out
-
-
-def gather_sparse_to_root(subs: torch.Tensor, vals: torch.Tensor, counts, root: int = 0):
-    """Optional gather of the distributed sparse result to ``root`` (timed separately:
-    bounded by the root's link ingress, SURVEY.md F6).  Returns (subs, vals) on root."""
-    rank, world = dist.get_rank(), dist.get_world_size()
-    nk = subs.shape[1] if subs.dim() == 2 else 1
-    if rank == root:
-        total = sum(counts)
-        all_s = torch.empty((total, nk), dtype=subs.dtype, device=subs.device)
-        all_v = torch.empty(total, dtype=vals.dtype, device=vals.device)
-        off = global_offsets(counts)
-        for r in range(world):
-            if r == root:
-                all_s[off[r]:off[r + 1]].copy_(subs[:counts[r]])
-                all_v[off[r]:off[r + 1]].copy_(vals[:counts[r]])
-            elif counts[r]:
-                dist.recv(all_s[off[r]:off[r + 1]], src=r)
-                dist.recv(all_v[off[r]:off[r + 1]], src=r)
-        return all_s, all_v
-    if counts[rank]:
-        dist.send(subs[:counts[rank]].contiguous(), dst=root)
-        dist.send(vals[:counts[rank]].contiguous(), dst=root)
-    return None, None

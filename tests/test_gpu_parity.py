@@ -593,7 +593,8 @@ def _ipc_worker(rank, world, port, q):
         vecs = {m: torch.rand(shape[m], dtype=torch.float64, device="cuda",
                               generator=torch.Generator(device="cuda").manual_seed(m)) for m in (1, 2, 3)}
         full = t.ttv_dense(vecs, 0).cpu().numpy()
-        merge = multi.PeerDenseMerge(shape[0], 0)
+        from gloo_comm import GlooComm
+        merge = multi.PeerDenseMerge(shape[0], 0, GlooComm())
         bounds = multi.shard_bounds(t.cols[0], world)
         lo, hi = multi.owned_key_range(t.cols[0], bounds, rank, shape[0])
         out = merge.run(t.slice(bounds[rank], bounds[rank + 1]), vecs, 0, lo, hi).cpu().numpy()
@@ -851,3 +852,39 @@ def test_tile_three_pass_fallback_bit_exact(oracle, monkeypatch, golden_small, g
         es, ev, _ = oracle.ttv_raw(subs, vals, shape, x, k)
         s, v, _ = K.ttv_raw(subs, vals, shape, x, k)
         assert s.tobytes() == es.tobytes() and v.tobytes() == ev.tobytes(), k
+
+
+def test_nccl_comm_inside_the_library_single_rank():
+    """The C-ABI NCCL data plane (tk_nccl_*) on the one GPU of the test box: a one-rank
+    communicator runs every exchange the sharded TTV uses -- the count all-gather (pipelined
+    tickets), the gather of sparse slices to the root, the IPC-handle exchange, the stream-ordered
+    barrier and the all-reduce merge -- and the peer-store dense merge driven through it."""
+    import torch
+    from paper_2510_01495_b200 import multi
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    comm = multi.NcclComm(0, 1, bootstrap=lambda uid: uid)
+    try:
+        t1, t2 = comm.counts_start(7), comm.counts_start(9)
+        assert comm.counts_wait(t1) == [7] and comm.counts_wait(t2) == [9]
+        s = torch.arange(10, dtype=torch.int64, device="cuda").reshape(5, 2)
+        v = torch.rand(5, dtype=torch.float64, device="cuda")
+        gs, gv = multi.gather_sparse_to_root(comm, s, v, [5])
+        assert torch.equal(gs, s) and torch.equal(gv, v)
+        assert comm.allgather_bytes(b"h" * 64) == [b"h" * 64]
+        x = torch.rand(1000, dtype=torch.float64, device="cuda")
+        y = x.clone()
+        multi.merge_dense(comm, y)
+        comm.barrier()
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        shape = (500, 30, 30, 30)
+        t = DeviceCoo.generate(shape, 200000, seed=12)
+        vecs = {m: uniform_vector(shape[m], 60 + m) for m in (1, 2, 3)}
+        full = t.ttv_dense(vecs, 0)
+        merge = multi.PeerDenseMerge(shape[0], torch.cuda.current_device(), comm)
+        out = merge.run(t, vecs, 0, 0, shape[0])
+        torch.cuda.synchronize()
+        assert torch.equal(out, full)
+        merge.close()
+    finally:
+        comm.close()

@@ -14,6 +14,8 @@ import torch.multiprocessing as mp
 
 from paper_2510_01495_b200 import multi
 
+from gloo_comm import GlooComm
+
 
 def _free_port():
     s = socket.socket()
@@ -50,16 +52,22 @@ def _worker(rank, world, port, result_q):
         assert bounds == multi.shard_bounds_np(key.numpy(), world)
         lo, hi = bounds[rank], bounds[rank + 1]
         s, v, _ = oracle.ttv_raw(subs[lo:hi], vals[lo:hi], shape, x, k)
-        counts = multi.gather_counts(len(v), torch.device("cpu"))
+        comm = GlooComm()
+        counts = multi.gather_counts(comm, len(v))
         off = multi.global_offsets(counts)
+        # the pipelined form the bench uses: start step i+1's gather before waiting on step i's
+        t1 = comm.counts_start(len(v))
+        t2 = comm.counts_start(2 * len(v))
+        assert comm.counts_wait(t1) == counts and comm.counts_wait(t2) == [2 * c for c in counts]
         # sparse gather to root (optional path)
-        all_s, all_v = multi.gather_sparse_to_root(torch.from_numpy(s.copy()), torch.from_numpy(v.copy()), counts)
+        all_s, all_v = multi.gather_sparse_to_root(comm, torch.from_numpy(s.copy()), torch.from_numpy(v.copy()), counts)
         # dense merge: keep mode 0, contract 1 and 2; shards split where the mode-0 index changes
         vecs = {1: np.random.default_rng(5).random(shape[1]), 2: np.random.default_rng(6).random(shape[2])}
         db = multi.shard_bounds(torch.from_numpy(subs[:, 0].copy()), world)
         lo, hi = db[rank], db[rank + 1]
         dense = oracle.ttv_multi_dense(subs[lo:hi], vals[lo:hi], shape, vecs, 0)
-        merged = multi.merge_dense(torch.from_numpy(dense.copy())).numpy()
+        merged = multi.merge_dense(comm, torch.from_numpy(dense.copy())).numpy()
+        assert comm.allgather_bytes(bytes([rank]) * 64) == [bytes([r]) * 64 for r in range(world)]
         if rank == 0:
             result_q.put(("ok", bounds, counts, off, all_s.numpy(), all_v.numpy(), merged))
     except Exception as exc:  # pragma: no cover - reported to the parent
