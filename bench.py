@@ -433,21 +433,31 @@ def secondary_measurements(rank, steps, threads, with_cpu):
     x5 = uniform_vector(c5["shape"][1], c5["xseed"] + 1)
     o_s5 = torch.empty((t5.nnz, 2), dtype=torch.int64, device="cuda")
     o_v5 = torch.empty(t5.nnz, dtype=torch.float64, device="cuda")
-    ts, u5 = [], 0
-    l0 = lib.tk_launch_count()
-    for i in range(3 + 2):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        u5 = t5.ttv(x5, 1, o_s5, o_v5)[0]
-        e1.record()
-        torch.cuda.synchronize()
-        if i >= 2:
-            ts.append(e0.elapsed_time(e1))
-    ms = float(np.median(ts))
+    def time_k1():
+        ts, u = [], 0
+        l0 = lib.tk_launch_count()
+        for i in range(3 + 2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            u = t5.ttv(x5, 1, o_s5, o_v5)[0]
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts)), u, (lib.tk_launch_count() - l0) / 5
+    ms, u5, launches = time_k1()  # the segmented counting path (tk_midmode.cu), no library sort
     b = c5["nnz"] * 32 + 8 * c5["shape"][1] + u5 * 24
     res["cfg5_ttv_mode1_sort_path"] = {"call_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c5["nnz"] / ms * 1e3,
-                                       "bytes": b, "u": u5, "launches_per_call": (lib.tk_launch_count() - l0) / 5}
+                                       "bytes": b, "u": u5, "launches_per_call": launches,
+                                       "path": "segmented counting by the suffix key (tk_midmode.cu)"}
+    os.environ["TK_MID_MODE"] = "0"  # the previous path, for comparison: CUB stable radix sort per interval
+    try:
+        ms0, _, launches0 = time_k1()
+    finally:
+        os.environ.pop("TK_MID_MODE", None)
+    res["cfg5_ttv_mode1_cub_split_path"] = {"call_ms": ms0, "GBps": b / ms0 / 1e6, "launches_per_call": launches0,
+                                            "path": "interval split + cub::DeviceRadixSort (TK_MID_MODE=0)"}
     del t5, o_s5, o_v5
     torch.cuda.empty_cache()
     return res

@@ -269,7 +269,7 @@ def shard_bounds(subs, nkeep: int, parts: int) -> list:
 
 def ttv_raw_threads(subs, vals, shape, x, k, threads: int = 0):
     """The reference's compiled ``ttv_raw`` (oracle/_ref; else the C port) over ``threads``
-    key-aligned shards of a canonical tensor whose contracted mode is the last one, each shard on
+    shards of a canonical tensor cut where the modes before ``k`` change, each shard on
     its own Python thread with the GIL released (``ttv_raw(..., release_gil=True)``,
     _ckernels.pyx:370-374).  The rank-order concatenation is the one-call result.  Returns
     ((subs, vals, shape), seconds, kind)."""
@@ -278,8 +278,10 @@ def ttv_raw_threads(subs, vals, shape, x, k, threads: int = 0):
     threads = int(threads or host_threads())
     ck = reference_module()
     kind = "reference" if ck is not None else "port"
-    d = len(shape)
-    bounds = shard_bounds(subs, d - 1, threads)
+    # the sorted key prefix of the kept tuple is the modes before k: cut shards where it changes
+    if int(k) == 0:
+        threads = 1
+    bounds = shard_bounds(subs, max(int(k), 1), threads)
 
     def run(i):
         lo, hi = bounds[i], bounds[i + 1]

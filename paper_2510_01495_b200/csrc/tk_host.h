@@ -76,6 +76,15 @@ int ttv_sparse_device(int d, const int64_t* shape, int64_t nnz, const int64_t* c
                       cudaStream_t st, bool keep_zeros = false);
 
 // dense-result multi-vector TTV (every mode except `keep` contracted).
+// Contracted mode 1 over canonical input (the paper's middle-mode protocol): segmented counting
+// by the suffix key (tk_midmode.cu).  Returns kMidDeclined when it does not apply.
+constexpr int kMidDeclined = -1;
+int ttv_middle_mode(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    const double* x, int64_t nx, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
+                    cudaStream_t st, bool keep_zeros);
+// stable removal of exact-zero groups from a (groups, nk) result (tk_ttv.cu)
+int compact_zeros(long long groups, int nk, long long* out_subs, double* out_vals, cudaStream_t st);
+
 int ttv_dense_device(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
                      int keep, const double* const* vecs, double* out, cudaStream_t st);
 

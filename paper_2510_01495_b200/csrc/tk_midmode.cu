@@ -1,0 +1,1077 @@
+// tk_midmode.cu -- general-mode TTV with the contracted mode second (k == 1): the paper's own
+// benchmark protocol contracts the middle mode (the reference CLI's
+// default --mode 2, pkg/src/tenkern/bench.py:69), so this is the sort path the workload hits.
+//
+// Reference semantics (_ckernels.pyx:313-367): w[r] = vals[r] * x[subs[r,1]]; rows grouped by
+// the kept tuple (i0, i2, ..., i_{d-1}); each group summed left to right in ASCENDING ORIGINAL ROW
+// ORDER (pyx:262-295); exact-zero sums dropped; groups emitted in lexicographic order.
+//
+// The input's leading column is sorted (canonical COO), so segment i0 (the rows with that
+// leading value) is already in place relative to the other segments: only a stable reorder by
+// the suffix key S = (i2, ..., i_{d-1}) (R = prod of those dims <= 2^14) WITHIN each segment is
+// needed.  That is a counting problem over small known dims -- no general sort.  Segments come in
+// three size classes:
+//   * class B (segments > kMedMax rows, the Zipf head): counting tiles of kTileRows rows.  Pass 1
+//     histograms S per tile in shared memory; a two-level column scan over each segment's tiles
+//     and a scan over S give every (tile, S) its exact row range; pass 2 recomputes w and scatters
+//     it stably -- the eight warps of a tile take 32-row steps in row order, ranks inside a step
+//     come from __match_any_sync, and the warps update the per-S cursors in turn (a token passed
+//     round a ring of named barriers), so every (i0, S) bucket holds its w in original row order;
+//     pass 3 folds every bucket serially (big buckets: coalesced warp loads several chunks ahead,
+//     one lane adds).
+//   * class M (kWin < rows <= kMedMax): one CTA per segment does the same in one tile, with the
+//     bucket cursors and starts in shared memory (no tables): a counting kernel before the output
+//     rows are known, the histogram + stable scatter + bucket folds after.
+//   * class A (segments <= kWin rows, the tail): one CTA per window of kWin class-A rows takes the
+//     class-A segments starting in it (<= 2 kWin rows), sorts their (segment, S) keys in shared
+//     memory with three stable LSD passes (the same token-ring scatter) and folds each group
+//     straight from the staged w; the groups go to a scratch indexed by class-A row and are moved
+//     to their final rows once the per-segment group counts are scanned.
+// Output rows: the groups of every segment (non-empty buckets / distinct S) are exclusive-scanned
+// over i0, so each group knows its output row without any cross-CTA wait.  Every fold is
+// acc = w[first]; acc = __dadd_rn(acc, w[next]) ... in original row order: values bit-identical to
+// the reference.  No library code is used.
+#include <algorithm>
+#include <vector>
+
+#include "tk_host.h"
+#include "tk_scan.cuh"
+
+namespace tk {
+
+// tk_ttv.cu
+__global__ void lead_offsets_kernel(long long n, const long long* __restrict__ col0, long long n0,
+                                    long long* __restrict__ off, Counters* ctr);
+
+namespace {
+
+constexpr int kMidThreads = 256;       // every kernel with a token ring: 8 warps
+constexpr int kMidWarps = kMidThreads / 32;
+constexpr int kWin = 2048;             // class A: segments of at most kWin rows; windows of kWin rows
+constexpr int kBufRows = 2 * kWin;     // rows of one class-A window (segments starting in it)
+constexpr long long kMidMaxR = 16384;  // suffix key S < 2^14
+constexpr int kChunkTiles = 32;        // column scan: tiles per chunk
+constexpr long long kMedMax = 65536;   // class M: segments of kWin+1 .. kMedMax rows
+constexpr long long kTileRows = 262144;  // class B counting tile (long runs per bucket: full-sector writes)
+constexpr int kMedBigList = kMedMax / 24;  // class M: warp-folded buckets of one segment
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// warp `warp`'s turn at step `step` of a ring of kMidWarps warps (ids 1..kMidWarps); the first turn
+// is free, and the last warp does not hand over after the last step
+__device__ __forceinline__ void ring_take(int warp, long long step) {
+  if (step > 0 || warp > 0) named_bar_sync(1 + warp, 64);
+}
+__device__ __forceinline__ void ring_pass(int warp, long long step, long long nstep) {
+  if (!(step == nstep - 1 && warp == kMidWarps - 1)) named_bar_arrive(1 + (warp + 1) % kMidWarps, 64);
+}
+
+struct MidParams {
+  long long nnz, n0, n1, R;
+  int ns;                          // suffix modes (d - 2)
+  int nk;                          // output columns (d - 1)
+  const long long* c0;             // leading kept column (sorted)
+  const long long* c1;             // contracted column
+  const long long* sc[kMaxKeep];   // suffix kept columns
+  long long sdim[kMaxKeep];
+  const double* vals;
+  const double* x;
+  const long long* off;            // n0 + 1 segment offsets
+  long long* out_subs;             // row-major (groups, nk)
+  double* out_vals;
+  const long long* out_base;       // n0 + 1: first output row of every segment
+  long long* groups;               // n0: groups of every segment
+  int* ti0;                        // class A scratch by class-A row (abase[i0] + rank): leading value,
+  unsigned int* tkey;              //   S of the segment's rank-th group
+  double* tval;                    //   and its value
+  const long long* abase;          // n0 + 1: first class-A row of every segment (class A only)
+  long long med_max;               // class M / class B boundary (rows)
+  Counters* ctr;
+};
+
+template <int NS>
+__device__ __forceinline__ long long suffix_key(const MidParams& p, long long r, unsigned int& flags) {
+  const int ns = NS > 0 ? NS : p.ns;
+  long long s = 0;
+  for (int j = 0; j < ns; ++j) {
+    const long long v = __ldg(p.sc[j] + r);
+    if ((unsigned long long)v >= (unsigned long long)p.sdim[j]) flags |= kFlagKeptOob;
+    s = s * p.sdim[j] + v;
+  }
+  return s;
+}
+
+__device__ __forceinline__ double row_w(const MidParams& p, long long r, unsigned int& flags) {
+  const long long i1 = __ldg(p.c1 + r);
+  const bool bad = (unsigned long long)i1 >= (unsigned long long)p.n1;
+  if (bad) flags |= kFlagIndex;
+  return __dmul_rn(__ldg(p.vals + r), __ldg(p.x + (bad ? 0 : i1)));
+}
+
+__device__ __forceinline__ void emit_group(const MidParams& p, long long g, long long i0, long long s, double v) {
+  long long* o = p.out_subs + g * p.nk;
+  o[0] = i0;
+  for (int j = p.ns - 1; j >= 0; --j) {
+    o[1 + j] = s % p.sdim[j];
+    s /= p.sdim[j];
+  }
+  p.out_vals[g] = v;
+}
+
+__device__ __forceinline__ void flush_counters(const MidParams& p, unsigned int flags, unsigned int zeros) {
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  zeros = __reduce_add_sync(0xffffffffu, zeros);
+  if ((threadIdx.x & 31) == 0) {
+    if (flags) atomicOr(&p.ctr->flags, flags);
+    if (zeros) atomicAdd(&p.ctr->zeros, (unsigned long long)zeros);
+  }
+}
+
+// Serial left fold of src[0..n) (acc = src[0]; acc = __dadd_rn(acc, src[1]) ...) by one warp: the
+// lanes load 32-value chunks kRingChunks chunks ahead and park each in a per-warp shared ring just
+// before it is needed; lane 0 adds in order from the ring (16-byte shared loads).  Lane 0's result.
+constexpr int kRingChunks = 8;
+
+__device__ __forceinline__ double warp_serial_fold(const double* __restrict__ src, long long n, double* ring) {
+  const int lane = threadIdx.x & 31;
+  double v[kRingChunks];
+#pragma unroll
+  for (int a = 0; a < kRingChunks; ++a) v[a] = a * 32 + lane < n ? src[a * 32 + lane] : 0.0;
+  double acc = 0.0;
+  const long long nch = (n + 31) / 32;
+  for (long long k = 0; k < nch; ++k) {
+    const int a = (int)(k % kRingChunks);
+    double cur = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRingChunks; ++q)
+      if (q == a) {
+        cur = v[q];
+        const long long nx = (k + kRingChunks) * 32 + lane;
+        v[q] = nx < n ? src[nx] : 0.0;  // in flight while lane 0 adds
+      }
+    ring[a * 32 + lane] = cur;
+    __syncwarp();
+    if (lane == 0) {
+      const double* c = ring + a * 32;
+      const int m = (int)min(32LL, n - k * 32);
+      int j = 0;
+      if (k == 0) {
+        acc = c[0];
+        j = 1;
+        if (m > 1) {
+          acc = __dadd_rn(acc, c[1]);
+          j = 2;
+        }
+      }
+      for (; j + 2 <= m; j += 2) {
+        const double2 pr = *reinterpret_cast<const double2*>(c + j);
+        acc = __dadd_rn(acc, pr.x);
+        acc = __dadd_rn(acc, pr.y);
+      }
+      if (j < m) acc = __dadd_rn(acc, c[j]);
+    }
+    __syncwarp();
+  }
+  return acc;
+}
+
+// ---- planning ---------------------------------------------------------------------------------
+// per segment: class-B flag, tile and chunk counts, class-M flag, class-A rows (all exclusive-scanned)
+__global__ void mid_classify_kernel(long long n0, const long long* __restrict__ off, long long tile_rows,
+                                    long long med_max, long long* __restrict__ isb, long long* __restrict__ ntile,
+                                    long long* __restrict__ nchunk, long long* __restrict__ ism,
+                                    long long* __restrict__ arows) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n0; i += (long long)gridDim.x * blockDim.x) {
+    const long long L = off[i + 1] - off[i];
+    const bool b = L > med_max;
+    const long long nt = b ? (L + tile_rows - 1) / tile_rows : 0;
+    isb[i] = b;
+    ntile[i] = nt;
+    nchunk[i] = (nt + kChunkTiles - 1) / kChunkTiles;
+    ism[i] = L > kWin && !b;
+    arows[i] = (L >= 1 && L <= kWin) ? L : 0;
+  }
+}
+
+// class-B and class-M segment lists (ascending i0), the segment of every class-B tile / chunk, and
+// the first segment of every class-A window (a segment belongs to the window its first class-A
+// row falls in)
+__global__ void mid_lists_kernel(long long n0, const long long* __restrict__ off, const long long* __restrict__ bidx,
+                                 const long long* __restrict__ tbase, const long long* __restrict__ cbase,
+                                 const long long* __restrict__ midx, const long long* __restrict__ abase,
+                                 int* __restrict__ blist, int* __restrict__ tile_seg, int* __restrict__ chunk_seg,
+                                 int* __restrict__ mlist, int* __restrict__ wfirst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n0; i += (long long)gridDim.x * blockDim.x) {
+    if (bidx[i + 1] != bidx[i]) {
+      blist[bidx[i]] = (int)i;
+      for (long long t = tbase[i]; t < tbase[i + 1]; ++t) tile_seg[t] = (int)i;
+      for (long long c = cbase[i]; c < cbase[i + 1]; ++c) chunk_seg[c] = (int)i;
+    }
+    if (midx[i + 1] != midx[i]) mlist[midx[i]] = (int)i;
+    if (abase[i + 1] != abase[i]) atomicMin(&wfirst[abase[i] / kWin], (int)i);
+  }
+}
+
+// Streams rows [r0, r1) in 256-row steps (warp w takes rows step*256 + 32w + lane) and scatters
+// w = vals * x[i1] stably to dst[cur[S]++] (token ring: the eight warps update the cursors in
+// turn, ranks inside a warp step from __match_any_sync).  The raw loads (S columns, i1, vals) are
+// issued kPipe steps ahead and the x gather one step ahead, so no instruction waits on a load
+// issued in the same step.
+constexpr int kPipe = 4;
+
+template <int NS>
+__device__ __forceinline__ void stream_scatter(const MidParams& p, long long r0, long long r1, unsigned int* cur,
+                                               double* __restrict__ dst, unsigned int& flags) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  const long long nstep = (r1 - r0 + kMidThreads - 1) / kMidThreads;
+  long long sq[kPipe], iq[kPipe];
+  double vq[kPipe];
+  auto load_raw = [&](long long r, long long& s, long long& i1, double& v) {
+    if (r < r1) {
+      s = suffix_key<NS>(p, r, flags);
+      i1 = __ldg(p.c1 + r);
+      v = __ldg(p.vals + r);
+    } else {
+      s = -1 - lane;
+      i1 = 0;
+      v = 0.0;
+    }
+  };
+  auto gather = [&](long long i1) {
+    const bool bad = (unsigned long long)i1 >= (unsigned long long)p.n1;
+    if (bad) flags |= kFlagIndex;
+    return __ldg(p.x + (bad ? 0 : i1));
+  };
+#pragma unroll
+  for (int a = 0; a < kPipe; ++a) load_raw(r0 + a * kMidThreads + warp * 32 + lane, sq[a], iq[a], vq[a]);
+  double xcur = gather(iq[0]);
+  for (long long step = 0; step < nstep; ++step) {
+    const int a = (int)(step % kPipe);
+    const long long r = r0 + step * kMidThreads + warp * 32 + lane;
+    long long s = 0, i1n = 0;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPipe; ++q) {  // static register indexing of the ring slots
+      if (q == a) {
+        s = sq[q];
+        v = vq[q];
+        load_raw(r + kPipe * kMidThreads, sq[q], iq[q], vq[q]);  // the step kPipe ahead
+      }
+      if (q == (a + 1) % kPipe) i1n = iq[q];
+    }
+    const double w = __dmul_rn(v, xcur);
+    xcur = gather(i1n);  // next step's x, in flight during this step's turn
+    const bool valid = r < r1 && (unsigned long long)s < (unsigned long long)p.R;
+    const unsigned int m = __match_any_sync(0xffffffffu, valid ? s : -1 - lane);
+    const unsigned int rank = __popc(m & lt);
+    ring_take(warp, step);
+    unsigned int pos = 0;
+    if (valid) pos = cur[s] + rank;
+    __syncwarp();
+    if (valid && rank == 0) cur[s] = pos + __popc(m);
+    __syncwarp();
+    ring_pass(warp, step, nstep);
+    if (valid) dst[pos] = w;
+  }
+}
+
+// ---- class B ----------------------------------------------------------------------------------
+// pass 1: histogram of S per tile -> H[t][S]
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_hist_kernel(MidParams p, long long tile_rows,
+                                                             const int* __restrict__ tile_seg,
+                                                             const long long* __restrict__ tbase,
+                                                             unsigned int* __restrict__ H) {
+  extern __shared__ unsigned int s_dyn[];
+  unsigned int* s_hist = s_dyn;
+  const long long t = blockIdx.x;
+  const int i0 = tile_seg[t];
+  const long long r0 = p.off[i0] + (t - tbase[i0]) * tile_rows;
+  const long long r1 = min(r0 + tile_rows, p.off[i0 + 1]);
+  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) s_hist[s] = 0;
+  __syncthreads();
+  unsigned int flags = 0;
+  for (long long r = r0 + threadIdx.x; r < r1; r += 4 * blockDim.x) {  // four loads in flight
+    long long s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = r + u * blockDim.x < r1 ? suffix_key<NS>(p, r + u * blockDim.x, flags) : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((unsigned long long)s[u] < (unsigned long long)p.R) atomicAdd(&s_hist[s[u]], 1u);
+  }
+  flush_counters(p, flags, 0);
+  __syncthreads();
+  unsigned int* h = H + t * p.R;
+  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) h[s] = s_hist[s];
+}
+
+// column scan, level 1: per chunk of kChunkTiles tiles, the sum of each S -> P[chunk][S]
+__global__ void mid_chunksum_kernel(long long R, const int* __restrict__ chunk_seg, const long long* __restrict__ tbase,
+                                    const long long* __restrict__ cbase, const unsigned int* __restrict__ H,
+                                    unsigned int* __restrict__ P) {
+  const long long c = blockIdx.x;
+  const long long s = (long long)blockIdx.y * blockDim.x + threadIdx.x;
+  if (s >= R) return;
+  const int i0 = chunk_seg[c];
+  const long long t0 = tbase[i0] + (c - cbase[i0]) * kChunkTiles;
+  const long long t1 = min(t0 + kChunkTiles, tbase[i0 + 1]);
+  unsigned int sum = 0;
+#pragma unroll 8
+  for (long long t = t0; t < t1; ++t) sum += H[t * R + s];
+  P[c * R + s] = sum;
+}
+
+// level 2: per class-B segment, exclusive scan of the chunk sums; TOT[b][S] = the segment's count
+__global__ void mid_chunkscan_kernel(long long R, const int* __restrict__ blist, const long long* __restrict__ cbase,
+                                     unsigned int* __restrict__ P, unsigned int* __restrict__ TOT) {
+  const long long b = blockIdx.x;
+  const long long s = (long long)blockIdx.y * blockDim.x + threadIdx.x;
+  if (s >= R) return;
+  const int i0 = blist[b];
+  unsigned int run = 0;
+  for (long long c = cbase[i0]; c < cbase[i0 + 1]; ++c) {
+    const unsigned int v = P[c * R + s];
+    P[c * R + s] = run;
+    run += v;
+  }
+  TOT[b * R + s] = run;
+}
+
+// level 3: H[t][S] -> exclusive prefix of S over the segment's earlier tiles
+__global__ void mid_chunkapply_kernel(long long R, const int* __restrict__ chunk_seg, const long long* __restrict__ tbase,
+                                      const long long* __restrict__ cbase, unsigned int* __restrict__ H,
+                                      const unsigned int* __restrict__ P) {
+  const long long c = blockIdx.x;
+  const long long s = (long long)blockIdx.y * blockDim.x + threadIdx.x;
+  if (s >= R) return;
+  const int i0 = chunk_seg[c];
+  const long long t0 = tbase[i0] + (c - cbase[i0]) * kChunkTiles;
+  const long long t1 = min(t0 + kChunkTiles, tbase[i0 + 1]);
+  unsigned int run = P[c * R + s];
+  for (long long t = t0; t < t1; ++t) {
+    const unsigned int v = H[t * R + s];
+    H[t * R + s] = run;
+    run += v;
+  }
+}
+
+// per class-B segment: bucket starts (exclusive scan of TOT over S) and group ranks (scan of the
+// non-empty flags); groups[i0] = the segment's non-empty buckets
+__global__ void __launch_bounds__(1024) mid_segscan_kernel(long long R, const int* __restrict__ blist,
+                                                           const unsigned int* __restrict__ TOT,
+                                                           unsigned int* __restrict__ BB, unsigned int* __restrict__ GR,
+                                                           long long* __restrict__ groups) {
+  __shared__ unsigned long long ws[33];
+  const long long b = blockIdx.x;
+  const unsigned int* tot = TOT + b * R;
+  const long long per = (R + blockDim.x - 1) / blockDim.x;
+  const long long a = min(R, (long long)threadIdx.x * per), e = min(R, a + per);
+  unsigned long long sum = 0;  // rows (low 32) | groups (high 32)
+  for (long long s = a; s < e; ++s) sum += (unsigned long long)tot[s] | ((unsigned long long)(tot[s] != 0) << 32);
+  unsigned long long total;
+  unsigned long long ex = block_excl_scan(sum, ws, &total);
+  for (long long s = a; s < e; ++s) {
+    BB[b * R + s] = (unsigned int)ex;
+    GR[b * R + s] = (unsigned int)(ex >> 32);
+    ex += (unsigned long long)tot[s] | ((unsigned long long)(tot[s] != 0) << 32);
+  }
+  if (threadIdx.x == 0) groups[blist[b]] = (long long)(total >> 32);
+}
+
+// pass 2: stable scatter of w into every bucket's row range, in original row order
+
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_scatter_kernel(MidParams p, long long tile_rows,
+                                                                const int* __restrict__ tile_seg,
+                                                                const long long* __restrict__ tbase,
+                                                                const long long* __restrict__ bidx,
+                                                                const unsigned int* __restrict__ H,
+                                                                const unsigned int* __restrict__ BB,
+                                                                double* __restrict__ wout) {
+  extern __shared__ unsigned int s_dyn[];
+  unsigned int* s_cur = s_dyn;  // per S: next output row (absolute)
+  const long long t = blockIdx.x;
+  const int i0 = tile_seg[t];
+  const long long r0 = p.off[i0] + (t - tbase[i0]) * tile_rows;
+  const long long r1 = min(r0 + tile_rows, p.off[i0 + 1]);
+  const long long b = bidx[i0];
+  const unsigned int seg0 = (unsigned int)p.off[i0];
+  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) s_cur[s] = seg0 + BB[b * p.R + s] + H[t * p.R + s];
+  __syncthreads();
+  unsigned int flags = 0;
+  stream_scatter<NS>(p, r0, r1, s_cur, wout, flags);
+  flush_counters(p, flags, 0);
+}
+
+// pass 3: fold every non-empty (i0, S) bucket.  Small buckets: one thread each; big ones are
+// queued for warp-cooperative folds.
+constexpr unsigned int kBigBucket = 64;
+
+__global__ void mid_fold_kernel(MidParams p, const int* __restrict__ blist, const unsigned int* __restrict__ TOT,
+                                const unsigned int* __restrict__ BB, const unsigned int* __restrict__ GR,
+                                const double* __restrict__ w, unsigned long long* __restrict__ bigq,
+                                unsigned int* __restrict__ bign) {
+  const long long b = blockIdx.x;
+  const long long s = (long long)blockIdx.y * blockDim.x + threadIdx.x;
+  unsigned int zeros = 0;
+  if (s < p.R) {
+    const unsigned int n = TOT[b * p.R + s];
+    if (n >= kBigBucket) {
+      const unsigned int q = atomicAdd(bign, 1u);
+      bigq[q] = ((unsigned long long)b << 32) | (unsigned long long)s;
+    } else if (n > 0) {
+      const int i0 = blist[b];
+      const long long start = p.off[i0] + BB[b * p.R + s];
+      double acc = w[start];
+      for (unsigned int j = 1; j < n; ++j) acc = __dadd_rn(acc, w[start + j]);
+      emit_group(p, p.out_base[i0] + GR[b * p.R + s], i0, s, acc);
+      zeros += acc == 0.0;
+    }
+  }
+  flush_counters(p, 0, zeros);
+}
+
+constexpr int kFoldAhead = 4;  // 32-row chunks of a big bucket in flight
+
+__global__ void __launch_bounds__(256) mid_fold_big_kernel(MidParams p, const int* __restrict__ blist,
+                                                           const unsigned int* __restrict__ TOT,
+                                                           const unsigned int* __restrict__ BB,
+                                                           const unsigned int* __restrict__ GR,
+                                                           const double* __restrict__ w,
+                                                           const unsigned long long* __restrict__ bigq,
+                                                           const unsigned int* __restrict__ bign) {
+  __shared__ __align__(16) double s_ring[8][kRingChunks * 32];
+  const int lane = threadIdx.x & 31;
+  const unsigned int nq = *bign;
+  const unsigned int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned int zeros = 0;
+  for (unsigned int q = gw; q < nq; q += nw) {
+    const unsigned long long e = bigq[q];
+    const long long b = (long long)(e >> 32);
+    const long long s = (long long)(e & 0xffffffffu);
+    const long long n = TOT[b * p.R + s];
+    const int i0 = blist[b];
+    const double acc = warp_serial_fold(w + p.off[i0] + BB[b * p.R + s], n, s_ring[threadIdx.x >> 5]);
+    if (lane == 0) {
+      emit_group(p, p.out_base[i0] + GR[b * p.R + s], i0, s, acc);
+      zeros += acc == 0.0;
+    }
+  }
+  flush_counters(p, 0, zeros);
+}
+
+// ---- class M: one CTA per segment -----------------------------------------------------------------
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_med_count_kernel(MidParams p, const int* __restrict__ mlist) {
+  extern __shared__ unsigned int s_dyn[];
+  unsigned int* hist = s_dyn;
+  __shared__ unsigned long long ws[33];
+  const int i0 = mlist[blockIdx.x];
+  const long long r0 = p.off[i0], r1 = p.off[i0 + 1];
+  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) hist[s] = 0;
+  __syncthreads();
+  unsigned int flags = 0;
+  for (long long r = r0 + threadIdx.x; r < r1; r += 4 * blockDim.x) {
+    long long s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = r + u * blockDim.x < r1 ? suffix_key<NS>(p, r + u * blockDim.x, flags) : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((unsigned long long)s[u] < (unsigned long long)p.R) atomicAdd(&hist[s[u]], 1u);
+  }
+  __syncthreads();
+  unsigned long long nz = 0;
+  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) nz += hist[s] != 0;
+  unsigned long long total;
+  block_excl_scan(nz, ws, &total);
+  if (threadIdx.x == 0) p.groups[i0] = (long long)total;
+  flush_counters(p, flags, 0);
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_med_kernel(MidParams p, const int* __restrict__ mlist,
+                                                            double* __restrict__ wout) {
+  extern __shared__ unsigned int s_dyn[];
+  unsigned int* start = s_dyn;      // per S: first row of the bucket (segment-relative)
+  unsigned int* cur = s_dyn + p.R;  // per S: next row to fill
+  __shared__ unsigned long long ws[33];
+  const int i0 = mlist[blockIdx.x];
+  const long long r0 = p.off[i0], r1 = p.off[i0 + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  unsigned int flags = 0, zeros = 0;
+  for (long long s = tid; s < p.R; s += blockDim.x) cur[s] = 0;
+  __syncthreads();
+  for (long long r = r0 + tid; r < r1; r += 4 * blockDim.x) {
+    long long s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = r + u * blockDim.x < r1 ? suffix_key<NS>(p, r + u * blockDim.x, flags) : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((unsigned long long)s[u] < (unsigned long long)p.R) atomicAdd(&cur[s[u]], 1u);
+  }
+  __syncthreads();
+  // bucket starts: exclusive scan of the counts over S, each thread a contiguous range of S
+  const long long per = (p.R + kMidThreads - 1) / kMidThreads;
+  const long long sa = min(p.R, (long long)tid * per), se = min(p.R, sa + per);
+  {
+    unsigned long long c = 0;
+    for (long long s = sa; s < se; ++s) c += cur[s];
+    unsigned long long total;
+    unsigned long long ex = block_excl_scan(c, ws, &total);
+    for (long long s = sa; s < se; ++s) {
+      const unsigned int n = cur[s];
+      start[s] = (unsigned int)ex;
+      cur[s] = (unsigned int)ex;
+      ex += n;
+    }
+  }
+  __syncthreads();
+  // stable scatter of w into the segment's rows of the scratch (token ring)
+  stream_scatter<NS>(p, r0, r1, cur, wout + r0, flags);
+  __syncthreads();  // the block's scattered w are visible to the block
+  // fold every non-empty bucket at its output row.  Ranks come from a scan over contiguous S
+  // ranges and are packed into start[] (rows and ranks < 2^16); the folds then take S striped
+  // over the threads (the Zipf-heavy small S spread out), buckets of >= kMedWarpFold rows queued
+  // for the warps (warp_serial_fold).
+  constexpr unsigned int kMedWarpFold = 24;
+  __shared__ unsigned int s_big[kMedBigList];
+  __shared__ unsigned int s_nbig;
+  __shared__ __align__(16) double s_ring[kMidWarps][kRingChunks * 32];
+  if (tid == 0) s_nbig = 0;
+  {
+    unsigned long long c = 0;
+    for (long long s = sa; s < se; ++s) c += cur[s] != start[s];
+    unsigned long long total;
+    unsigned int g = (unsigned int)block_excl_scan(c, ws, &total);
+    for (long long s = sa; s < se; ++s)
+      if (cur[s] != start[s]) start[s] |= (g++) << 16;
+  }
+  __syncthreads();
+  const long long gbase = p.out_base[i0];
+  const double* src = wout + r0;
+  for (long long s = tid; s < p.R; s += kMidThreads) {
+    const unsigned int st0 = start[s], a0 = st0 & 0xffffu, e = cur[s];
+    if (a0 == e) continue;
+    if (e - a0 >= kMedWarpFold) {
+      s_big[atomicAdd(&s_nbig, 1u)] = (unsigned int)s;
+      continue;
+    }
+    double acc = src[a0];
+    unsigned int j = a0 + 1;
+    for (; j + 4 <= e; j += 4) {  // independent loads ahead of the dependent adds
+      const double v0 = src[j], v1 = src[j + 1], v2 = src[j + 2], v3 = src[j + 3];
+      acc = __dadd_rn(acc, v0);
+      acc = __dadd_rn(acc, v1);
+      acc = __dadd_rn(acc, v2);
+      acc = __dadd_rn(acc, v3);
+    }
+    for (; j < e; ++j) acc = __dadd_rn(acc, src[j]);
+    emit_group(p, gbase + (st0 >> 16), i0, s, acc);
+    zeros += acc == 0.0;
+  }
+  __syncthreads();
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    const unsigned int nbig = s_nbig;
+    for (unsigned int k = warp; k < nbig; k += kMidWarps) {
+      const long long s = s_big[k];
+      const unsigned int st0 = start[s], a0 = st0 & 0xffffu;
+      const double acc = warp_serial_fold(src + a0, cur[s] - a0, s_ring[warp]);
+      if (lane == 0) {
+        emit_group(p, gbase + (st0 >> 16), i0, s, acc);
+        zeros += acc == 0.0;
+      }
+    }
+  }
+  flush_counters(p, flags, zeros);
+}
+
+// ---- class A: one CTA per window of kWin class-A rows ------------------------------------------
+struct WinSmem {
+  unsigned int key[2][kBufRows];      // seg_local << 14 | S
+  unsigned short li[2][kBufRows];     // local row (stable payload)
+  double w[kBufRows];                 // w by local row
+  union {
+    int seg_row0[kWin];                 // first row of every segment, while keys are built
+    unsigned short hw[kMidWarps][512];  // per-warp digit counts, then cursors, while sorting
+  };
+  int seg_i0[kWin];                   // class-A segments starting in the window
+  union {
+    int seg_base[kWin + 1];           // their first local row (exclusive scan), while keys are built
+    int seg_g0[kWin + 1];             // their first group (window-local), while groups are folded
+  };
+  unsigned long long ws[33];
+  int nseg, nrows, first;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_window_kernel(MidParams p, const int* __restrict__ wfirst,
+                                                               long long nwin) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  WinSmem& S = *reinterpret_cast<WinSmem*>(s_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  unsigned int flags = 0, zeros = 0;
+  // candidate segments: from this window's first class-A segment to the next window's
+  // (only the last window can hold no segment start: a class-A segment is shorter than a window,
+  // so it covers a whole window only when that window is cut short by the end of the rows)
+  const int first = wfirst[blockIdx.x];
+  if (first >= p.n0) return;
+  const int nxt = blockIdx.x + 1 < nwin ? wfirst[blockIdx.x + 1] : (int)p.n0;
+  const int cand = min(nxt, (int)p.n0) - first;
+  // class-A ones (1 <= L <= kWin), compacted in order; their rows concatenated.  Empty segments
+  // also "start" in the window, so the candidates come in rounds of kWin (at most kWin of them
+  // are non-empty: they start at distinct rows of the window).
+  int nseg_run = 0, nrows_run = 0;
+  for (int cb = 0; cb < cand; cb += kWin) {
+    constexpr int PER = kWin / kMidThreads;
+    int inc[PER], len[PER];
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int c = cb + tid * PER + j;
+      len[j] = 0;
+      inc[j] = 0;
+      if (c < cand) {
+        const long long L = p.off[first + c + 1] - p.off[first + c];
+        if (L >= 1 && L <= kWin) {
+          inc[j] = 1;
+          len[j] = (int)L;
+        }
+      }
+      tot += ((unsigned long long)inc[j] << 32) | (unsigned long long)len[j];
+    }
+    unsigned long long total;
+    unsigned long long ex = block_excl_scan(tot, S.ws, &total);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (inc[j]) {
+        const int k = nseg_run + (int)(ex >> 32);
+        S.seg_i0[k] = first + cb + tid * PER + j;
+        S.seg_base[k] = nrows_run + (int)(ex & 0xffffffffu);
+        S.seg_row0[k] = (int)p.off[first + cb + tid * PER + j];
+      }
+      ex += ((unsigned long long)inc[j] << 32) | (unsigned long long)len[j];
+    }
+    nseg_run += (int)(total >> 32);
+    nrows_run += (int)(total & 0xffffffffu);
+  }
+  if (tid == 0) {
+    S.nseg = nseg_run;
+    S.nrows = nrows_run;
+    S.seg_base[nseg_run] = nrows_run;
+  }
+  __syncthreads();
+  const int nseg = S.nseg, n = S.nrows;
+  if (nseg == 0) return;
+  // keys and w, local row by local row (coalesced within a segment); four rows per thread in
+  // flight: raw loads first, then the x gathers
+  for (int l0 = tid; l0 < n; l0 += 8 * kMidThreads) {
+    long long r[8], sk[8], i1[8];
+    double v[8];
+    int sl[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int li = l0 + u * kMidThreads;
+      sl[u] = 0;
+      r[u] = -1;
+      if (li < n) {
+        int lo = 0, hi = nseg - 1;  // segment of local row li: last base <= li
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (S.seg_base[mid] <= li) lo = mid;
+          else hi = mid - 1;
+        }
+        sl[u] = lo;
+        r[u] = S.seg_row0[lo] + (li - S.seg_base[lo]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (r[u] < 0) continue;
+      sk[u] = suffix_key<NS>(p, r[u], flags);
+      i1[u] = __ldg(p.c1 + r[u]);
+      v[u] = __ldg(p.vals + r[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (r[u] < 0) continue;
+      const int li = l0 + u * kMidThreads;
+      const bool bad = (unsigned long long)i1[u] >= (unsigned long long)p.n1;
+      if (bad) flags |= kFlagIndex;
+      S.w[li] = __dmul_rn(v[u], __ldg(p.x + (bad ? 0 : i1[u])));
+      S.key[0][li] = ((unsigned int)sl[u] << 14) | (unsigned int)max(0LL, min(sk[u], p.R - 1));
+      S.li[0][li] = (unsigned short)li;
+    }
+  }
+  __syncthreads();
+  // three stable LSD passes over the 25-bit (seg_local, S) key, 9-bit digits.  Each warp owns a
+  // contiguous block of the keys: per-warp digit counts, one scan over (digit, warp), then every
+  // warp scatters its block in order with its own cursors -- no cross-warp ordering needed.
+  int cur = 0;
+  const int blk = (n + kMidWarps - 1) / kMidWarps;
+  const int b0 = min(n, warp * blk), b1 = min(n, b0 + blk);
+  for (int shift = 0; shift < 27; shift += 9) {
+    for (int i = lane; i < 512; i += 32) S.hw[warp][i] = 0;
+    __syncwarp();
+    for (int i0c = b0; i0c < b1; i0c += 32) {
+      const int i = i0c + lane;
+      const unsigned int dg = i < b1 ? (S.key[cur][i] >> shift) & 511u : 512u + lane;
+      const unsigned int m = __match_any_sync(0xffffffffu, dg);
+      if (i < b1 && (m & lt) == 0) S.hw[warp][dg] += (unsigned short)__popc(m);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // cursor of (warp, digit) = all keys of smaller digits + this digit's keys in earlier warps
+      unsigned int c[2][kMidWarps], tot2 = 0;
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int w8 = 0; w8 < kMidWarps; ++w8) {
+          c[d][w8] = S.hw[w8][2 * tid + d];
+          tot2 += c[d][w8];
+        }
+      unsigned long long total;
+      unsigned int run = (unsigned int)block_excl_scan((unsigned long long)tot2, S.ws, &total);
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int w8 = 0; w8 < kMidWarps; ++w8) {
+          S.hw[w8][2 * tid + d] = (unsigned short)run;
+          run += c[d][w8];
+        }
+    }
+    __syncthreads();
+    for (int i0c = b0; i0c < b1; i0c += 32) {
+      const int i = i0c + lane;
+      const bool valid = i < b1;
+      const unsigned int key = valid ? S.key[cur][i] : 0u;
+      const unsigned short l = valid ? S.li[cur][i] : 0;
+      const unsigned int dg = valid ? (key >> shift) & 511u : 512u + lane;
+      const unsigned int m = __match_any_sync(0xffffffffu, dg);
+      const unsigned int rank = __popc(m & lt);
+      unsigned int pos = 0;
+      if (valid) pos = S.hw[warp][dg] + rank;
+      __syncwarp();
+      if (valid && rank == 0) S.hw[warp][dg] = (unsigned short)(pos + __popc(m));
+      __syncwarp();
+      if (valid) {
+        S.key[cur ^ 1][pos] = key;
+        S.li[cur ^ 1][pos] = l;
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  // groups: runs of equal key; heads -> window-local group ids (block scan), segment first groups
+  const unsigned int* K = S.key[cur];
+  int* hp = reinterpret_cast<int*>(S.key[cur ^ 1]);  // head positions by group id (free buffer)
+  {
+    constexpr int PER = kBufRows / kMidThreads;
+    unsigned long long cnt = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = tid * PER + j;
+      cnt += (i < n && (i == 0 || K[i] != K[i - 1])) ? 1ull : 0ull;
+    }
+    unsigned long long total;
+    unsigned long long g = block_excl_scan(cnt, S.ws, &total);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = tid * PER + j;
+      if (i < n && (i == 0 || K[i] != K[i - 1])) {
+        hp[g] = i;
+        if (i == 0 || (K[i] >> 14) != (K[i - 1] >> 14)) S.seg_g0[K[i] >> 14] = (int)g;
+        ++g;
+      }
+    }
+    if (tid == 0) hp[total] = n;
+    __syncthreads();
+    const int ng = (int)total;
+    for (int k = tid; k < nseg; k += kMidThreads) {
+      const int gend = k + 1 < nseg ? S.seg_g0[k + 1] : ng;
+      p.groups[S.seg_i0[k]] = gend - S.seg_g0[k];
+    }
+    // fold every group (one thread each), into the row-indexed scratch of its segment
+    for (int g2 = tid; g2 < ng; g2 += kMidThreads) {
+      const int a = hp[g2], e = hp[g2 + 1];
+      const unsigned int key = K[a];
+      const int sl = (int)(key >> 14);
+      double acc = S.w[S.li[cur][a]];
+      for (int i = a + 1; i < e; ++i) acc = __dadd_rn(acc, S.w[S.li[cur][i]]);
+      const int i0 = S.seg_i0[sl];
+      const long long row = p.abase[i0] + (g2 - S.seg_g0[sl]);
+      p.ti0[row] = i0;
+      p.tkey[row] = key & 0x3fffu;
+      p.tval[row] = acc;
+      zeros += acc == 0.0;
+    }
+  }
+  flush_counters(p, flags, zeros);
+}
+
+// class-A groups: scratch (by class-A row; unwritten slots hold -1) -> final rows, thread per slot
+__global__ void mid_move_kernel(MidParams p, long long na) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < na; j += (long long)gridDim.x * blockDim.x) {
+    const int i0 = p.ti0[j];
+    if (i0 < 0) continue;
+    emit_group(p, p.out_base[i0] + (j - p.abase[i0]), i0, p.tkey[j], p.tval[j]);
+  }
+}
+
+int mid_grid(long long n) { return (int)std::max(1LL, std::min((n + 255) / 256, (long long)num_sms() * 16)); }
+
+long long env_ll(const char* name, long long dflt) {
+  const char* e = getenv(name);
+  return e ? std::max(1LL, atoll(e)) : dflt;
+}
+
+template <int NS>
+int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
+  const long long n0 = p.n0, R = p.R, nnz = p.nnz;
+  // tests shrink these to put small data through every class and many tiles
+  const long long tile_rows = env_ll("TK_MID_TILE", kTileRows);
+  p.med_max = std::min(kMedMax, std::max<long long>(kWin, env_ll("TK_MID_MEDMAX", kMedMax)));
+  long long* hv = static_cast<long long*>(pinned_scratch(sizeof(Counters) + 96));
+  Counters* hc = reinterpret_cast<Counters*>(hv + 8);
+  DevBuf b_ctr, b_off, b_plan, b_groups;
+  if (int rc = b_ctr.alloc(sizeof(Counters), st)) return rc;
+  p.ctr = b_ctr.as<Counters>();
+  TK_CUDA(cudaMemsetAsync(p.ctr, 0, sizeof(Counters), st));
+  if (int rc = b_off.alloc((size_t)(n0 + 1) * 8, st)) return rc;
+  lead_offsets_kernel<<<mid_grid(nnz), 256, 0, st>>>(nnz, p.c0, n0, b_off.as<long long>(), p.ctr);
+  p.off = b_off.as<long long>();
+  if (int rc = b_plan.alloc((size_t)(n0 + 1) * 8 * 5, st)) return rc;
+  long long* isb = b_plan.as<long long>();  // -> bidx
+  long long* tbase = isb + (n0 + 1);
+  long long* cbase = tbase + (n0 + 1);
+  long long* midx = cbase + (n0 + 1);
+  long long* abase = midx + (n0 + 1);
+  mid_classify_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, p.off, tile_rows, p.med_max, isb, tbase, cbase, midx, abase);
+  count_launch(2);
+  TK_CUDA(cudaGetLastError());
+  for (long long* a : {isb, tbase, cbase, midx, abase})
+    if (int rc = scan_excl_i64(a, a, n0, st)) return rc;  // [n0] = the totals
+  TK_CUDA(cudaMemcpyAsync(hc, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  int j = 0;
+  for (long long* a : {isb, tbase, cbase, midx, abase}) TK_CUDA(cudaMemcpyAsync(hv + j++, a + n0, 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (hc->flags) return kMidDeclined;  // unsorted or out-of-range leading column
+  const long long nb = hv[0], ntiles = hv[1], nchunks = hv[2], nm = hv[3], na = hv[4];
+  const long long nwin = (na + kWin - 1) / kWin;
+  p.abase = abase;
+
+  if (int rc = b_groups.alloc((size_t)(n0 + 1) * 8, st)) return rc;
+  TK_CUDA(cudaMemsetAsync(b_groups.get(), 0, (size_t)(n0 + 1) * 8, st));
+  p.groups = b_groups.as<long long>();
+  DevBuf b_lists, b_H, b_P, b_TOT, b_BB, b_GR, b_w, b_bigq, b_bign, b_ti0, b_tkey, b_tval;
+  if (int rc = b_lists.alloc((size_t)(nb + ntiles + nchunks + nm + nwin + 4) * 4, st)) return rc;
+  int* blist = b_lists.as<int>();
+  int* tseg = blist + nb;
+  int* cseg = tseg + ntiles;
+  int* mlist = cseg + nchunks;
+  int* wfirst = mlist + nm;
+  TK_CUDA(cudaMemsetAsync(wfirst, 0x7f, (size_t)(nwin + 1) * 4, st));
+  mid_lists_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, p.off, isb, tbase, cbase, midx, abase, blist, tseg, cseg, mlist,
+                                                 wfirst);
+  count_launch();
+  const dim3 blk(256);
+  const unsigned int ry = (unsigned int)((R + 255) / 256);
+  const size_t hsm = (size_t)R * 4;
+  // ---- class B: tiles, column scans, bucket starts / group ranks / group counts
+  if (nb > 0) {
+    if (int rc = b_H.alloc((size_t)ntiles * R * 4, st)) return rc;
+    if (int rc = b_P.alloc((size_t)nchunks * R * 4, st)) return rc;
+    if (int rc = b_TOT.alloc((size_t)nb * R * 4, st)) return rc;
+    if (int rc = b_BB.alloc((size_t)nb * R * 4, st)) return rc;
+    if (int rc = b_GR.alloc((size_t)nb * R * 4, st)) return rc;
+    TK_CUDA(cudaFuncSetAttribute(mid_hist_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    TK_CUDA(cudaFuncSetAttribute(mid_scatter_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    mid_hist_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm, st>>>(p, tile_rows, tseg, tbase, b_H.as<unsigned int>());
+    mid_chunksum_kernel<<<dim3((unsigned int)nchunks, ry), blk, 0, st>>>(R, cseg, tbase, cbase, b_H.as<unsigned int>(),
+                                                                         b_P.as<unsigned int>());
+    mid_chunkscan_kernel<<<dim3((unsigned int)nb, ry), blk, 0, st>>>(R, blist, cbase, b_P.as<unsigned int>(),
+                                                                     b_TOT.as<unsigned int>());
+    mid_chunkapply_kernel<<<dim3((unsigned int)nchunks, ry), blk, 0, st>>>(R, cseg, tbase, cbase, b_H.as<unsigned int>(),
+                                                                           b_P.as<unsigned int>());
+    mid_segscan_kernel<<<(unsigned int)nb, 1024, 0, st>>>(R, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
+                                                          b_GR.as<unsigned int>(), p.groups);
+    count_launch(5);
+  }
+  // ---- class M: group counts
+  if (nm > 0) {
+    TK_CUDA(cudaFuncSetAttribute(mid_med_count_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    mid_med_count_kernel<NS><<<(unsigned int)nm, kMidThreads, hsm, st>>>(p, mlist);
+    count_launch();
+  }
+  // ---- class A: windows -> scratch by class-A row + group counts
+  if (nwin > 0) {
+    if (int rc = b_ti0.alloc((size_t)na * 4, st)) return rc;
+    if (int rc = b_tkey.alloc((size_t)na * 4, st)) return rc;
+    if (int rc = b_tval.alloc((size_t)na * 8, st)) return rc;
+    p.ti0 = b_ti0.as<int>();
+    p.tkey = b_tkey.as<unsigned int>();
+    p.tval = b_tval.as<double>();
+    TK_CUDA(cudaMemsetAsync(p.ti0, 0xff, (size_t)na * 4, st));
+    TK_CUDA(cudaFuncSetAttribute(mid_window_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(WinSmem)));
+    mid_window_kernel<NS><<<(unsigned int)nwin, kMidThreads, sizeof(WinSmem), st>>>(p, wfirst, nwin);
+    count_launch();
+  }
+  TK_CUDA(cudaGetLastError());
+  if (int rc = scan_excl_i64(p.groups, p.groups, n0, st)) return rc;  // -> out_base, [n0] = groups
+  p.out_base = p.groups;
+  // ---- class B and M: scatter + folds straight to the output rows; class A: the move
+  if (nb > 0 || nm > 0)
+    if (int rc = b_w.alloc((size_t)nnz * 8, st)) return rc;
+  if (nb > 0) {
+    if (int rc = b_bigq.alloc(((size_t)nnz / kBigBucket + 64) * 8, st)) return rc;
+    if (int rc = b_bign.alloc(16, st)) return rc;
+    TK_CUDA(cudaMemsetAsync(b_bign.get(), 0, 16, st));
+    mid_scatter_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm, st>>>(
+        p, tile_rows, tseg, tbase, isb, b_H.as<unsigned int>(), b_BB.as<unsigned int>(), b_w.as<double>());
+    mid_fold_kernel<<<dim3((unsigned int)nb, ry), blk, 0, st>>>(p, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
+                                                                b_GR.as<unsigned int>(), b_w.as<double>(),
+                                                                b_bigq.as<unsigned long long>(), b_bign.as<unsigned int>());
+    mid_fold_big_kernel<<<num_sms() * 8, 256, 0, st>>>(p, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
+                                                       b_GR.as<unsigned int>(), b_w.as<double>(),
+                                                       b_bigq.as<unsigned long long>(), b_bign.as<unsigned int>());
+    count_launch(3);
+  }
+  if (nm > 0) {
+    TK_CUDA(cudaFuncSetAttribute(mid_med_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * hsm)));
+    mid_med_kernel<NS><<<(unsigned int)nm, kMidThreads, 2 * hsm, st>>>(p, mlist, b_w.as<double>());
+    count_launch();
+  }
+  if (na > 0) {
+    mid_move_kernel<<<mid_grid(na), 256, 0, st>>>(p, na);
+    count_launch();
+  }
+  TK_CUDA(cudaGetLastError());
+  TK_CUDA(cudaMemcpyAsync(hc, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaMemcpyAsync(hv + 5, p.groups + n0, 8, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  const long long G = hv[5];
+  if (hc->flags & kFlagIndex) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "ttv: mode-1 index out of range for a vector of length %lld", p.n1);
+    return fail(TK_EINDEX, buf);
+  }
+  if (hc->flags & kFlagKeptOob) return kMidDeclined;  // garbage kept indices: the LSD path
+  if (keep_zeros) {
+    *out_nnz = G;
+    return TK_OK;
+  }
+  if (hc->zeros) {
+    if (int rc = compact_zeros(G, p.nk, p.out_subs, p.out_vals, st)) return rc;
+    TK_CUDA(cudaStreamSynchronize(st));
+  }
+  *out_nnz = G - (long long)hc->zeros;
+  return TK_OK;
+}
+
+}  // namespace
+
+int ttv_middle_mode(int d, const int64_t* shape, int64_t nnz, const int64_t* const* cols, const double* vals,
+                    const double* x, int64_t nx, int64_t* out_subs, double* out_vals, int64_t* out_nnz,
+                    cudaStream_t st, bool keep_zeros) {
+  if (d < 3 || nnz <= 0 || nnz >= (1LL << 31) || shape[0] > (1LL << 24)) return kMidDeclined;
+  long long R = 1;
+  for (int m = 2; m < d; ++m) {
+    R *= shape[m];
+    if (R > kMidMaxR) return kMidDeclined;
+  }
+  MidParams p{};
+  p.nnz = nnz;
+  p.n0 = shape[0];
+  p.n1 = nx;
+  p.R = R;
+  p.ns = d - 2;
+  p.nk = d - 1;
+  p.c0 = reinterpret_cast<const long long*>(cols[0]);
+  p.c1 = reinterpret_cast<const long long*>(cols[1]);
+  for (int m = 2; m < d; ++m) {
+    p.sc[m - 2] = reinterpret_cast<const long long*>(cols[m]);
+    p.sdim[m - 2] = shape[m];
+  }
+  p.vals = vals;
+  p.x = x;
+  p.out_subs = reinterpret_cast<long long*>(out_subs);
+  p.out_vals = out_vals;
+  *out_nnz = 0;
+  return d == 3 ? mid_run<1>(p, keep_zeros, out_nnz, st) : mid_run<0>(p, keep_zeros, out_nnz, st);
+}
+
+// ---- device-wide exclusive scan (tk_scan.cuh) --------------------------------------------------
+namespace {
+constexpr int kScanThreads = 1024, kScanItems = 4, kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums_kernel(const long long* __restrict__ in, long long n,
+                                                                      long long* __restrict__ sums) {
+  __shared__ long long ws[33];
+  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  long long v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v += base + i < n ? in[base + i] : 0;
+  long long tot;
+  block_excl_scan(v, ws, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(long long* __restrict__ sums, long long nt) {
+  __shared__ long long ws[33];
+  const long long per = (nt + kScanThreads - 1) / kScanThreads;
+  const long long a = min(nt, (long long)threadIdx.x * per), e = min(nt, a + per);
+  long long v = 0;
+  for (long long i = a; i < e; ++i) v += sums[i];
+  long long tot;
+  long long ex = block_excl_scan(v, ws, &tot);
+  for (long long i = a; i < e; ++i) {
+    const long long c = sums[i];
+    sums[i] = ex;
+    ex += c;
+  }
+  if (threadIdx.x == 0) sums[nt] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const long long* in, long long* out, long long n,
+                                                                  const long long* __restrict__ sums) {
+  __shared__ long long ws[33];
+  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  long long v[kScanItems], s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    s += v[i];
+  }
+  long long tot;
+  long long ex = block_excl_scan(s, ws, &tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = ex;
+    ex += v[i];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+}
+}  // namespace
+
+int scan_excl_i64(const long long* in, long long* out, long long n, cudaStream_t st) {
+  const long long nt = std::max(1LL, (n + kScanTile - 1) / kScanTile);
+  DevBuf sums;
+  if (int rc = sums.alloc((size_t)(nt + 1) * 8, st)) return rc;
+  scan_tile_sums_kernel<<<(unsigned int)nt, kScanThreads, 0, st>>>(in, n, sums.as<long long>());
+  scan_sums_kernel<<<1, kScanThreads, 0, st>>>(sums.as<long long>(), nt);
+  scan_apply_kernel<<<(unsigned int)nt, kScanThreads, 0, st>>>(in, out, n, sums.as<long long>());
+  count_launch(3);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+}  // namespace tk

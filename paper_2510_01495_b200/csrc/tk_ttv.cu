@@ -770,23 +770,6 @@ int run_seg(int src, SegParams& p, cudaStream_t st, Counters* host_ctr) {
   return TK_OK;
 }
 
-int compact_zeros(long long groups, int nk, long long* out_subs, double* out_vals, cudaStream_t st) {
-  const long long nblk = (groups + kCompTile - 1) / kCompTile;
-  DevBuf blk, v2, s2;
-  if (int rc = blk.alloc(nblk * 8, st)) return rc;
-  if (int rc = v2.alloc(groups * 8, st)) return rc;
-  if (int rc = s2.alloc(groups * 8 * std::max(nk, 1), st)) return rc;
-  nz_count_kernel<<<(unsigned)nblk, 256, 0, st>>>(groups, out_vals, blk.as<long long>());
-  scan_blocks_kernel<<<1, 256, 0, st>>>(nblk, blk.as<long long>());
-  nz_scatter_kernel<<<(unsigned)nblk, 256, 0, st>>>(groups, nk, out_vals, out_subs, blk.as<long long>(),
-                                                    v2.as<double>(), s2.as<long long>());
-  count_launch(3);
-  TK_CUDA(cudaGetLastError());
-  TK_CUDA(cudaMemcpyAsync(out_vals, v2.get(), groups * 8, cudaMemcpyDeviceToDevice, st));
-  TK_CUDA(cudaMemcpyAsync(out_subs, s2.get(), groups * 8 * nk, cudaMemcpyDeviceToDevice, st));
-  return TK_OK;
-}
-
 int finish(const Counters& c, int k, long long nx, int nk, long long* out_subs, double* out_vals,
            int64_t* out_nnz, cudaStream_t st, bool keep_zeros = false) {
   if (c.flags & kFlagIndex) {
@@ -984,6 +967,12 @@ int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const
     const char* e = getenv("TK_SPLIT_SORT");
     return e && e[0] == '0';
   }();
+  // TK_MID_MODE=0 in the environment disables the middle-mode counting path (parity tests)
+  const char* mm = getenv("TK_MID_MODE");
+  if (k == 1 && !(mm && mm[0] == '0')) {
+    const int rc = ttv_middle_mode(d, shape, nnz, cols, vals, x, nx, out_subs, out_vals, out_nnz, st, keep_zeros);
+    if (rc != kMidDeclined) return rc;
+  }
   if (linear && k != 0 && TK_SPLIT_SORT && !split_env_off) {
     const int rc = ttv_general_split(nnz, nk, kc, dims, cols, vals, x, nx, k, out_subs, out_vals, out_nnz, st,
                                      keep_zeros);
@@ -1063,6 +1052,24 @@ int ttv_general(int d, const int64_t* shape, long long nnz, const int64_t* const
 }
 
 }  // namespace
+
+int compact_zeros(long long groups, int nk, long long* out_subs, double* out_vals, cudaStream_t st) {
+  const long long nblk = (groups + kCompTile - 1) / kCompTile;
+  DevBuf blk, v2, s2;
+  if (int rc = blk.alloc(nblk * 8, st)) return rc;
+  if (int rc = v2.alloc(groups * 8, st)) return rc;
+  if (int rc = s2.alloc(groups * 8 * std::max(nk, 1), st)) return rc;
+  nz_count_kernel<<<(unsigned)nblk, 256, 0, st>>>(groups, out_vals, blk.as<long long>());
+  scan_blocks_kernel<<<1, 256, 0, st>>>(nblk, blk.as<long long>());
+  nz_scatter_kernel<<<(unsigned)nblk, 256, 0, st>>>(groups, nk, out_vals, out_subs, blk.as<long long>(),
+                                                    v2.as<double>(), s2.as<long long>());
+  count_launch(3);
+  TK_CUDA(cudaGetLastError());
+  TK_CUDA(cudaMemcpyAsync(out_vals, v2.get(), groups * 8, cudaMemcpyDeviceToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(out_subs, s2.get(), groups * 8 * nk, cudaMemcpyDeviceToDevice, st));
+  return TK_OK;
+}
+
 
 int ttv_prefix_try(int d, int64_t nnz, const int64_t* const* cols, const double* vals, const double* x, int64_t nx,
                    int64_t* out_subs, double* out_vals, int64_t* out_nnz, bool* unsorted, cudaStream_t st) {

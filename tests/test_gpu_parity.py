@@ -888,3 +888,79 @@ def test_nccl_comm_inside_the_library_single_rank():
         merge.close()
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("shape,nnz,zipf,env", [
+    ((400, 300, 200), 600_000, 1.3, {}),                             # Zipf: classes A, M and B at once
+    ((50, 300, 200), 2_000_000, 1.2, {}),                            # class B + M segments
+    ((20, 200, 200), 500_000, 0.0, {}),                              # class M only (25K-row segments)
+    ((60, 80, 90), 200_000, 1.1, {"TK_MID_TILE": "97", "TK_MID_MEDMAX": "2048"}),  # many B tiles + chunks
+    ((30, 40, 20, 10), 150_000, 1.2, {"TK_MID_TILE": "257", "TK_MID_MEDMAX": "2048"}),  # order 4
+    ((30, 40, 20, 10), 150_000, 1.2, {}),                            # order 4, class M
+    ((3000, 20, 30), 400_000, 0.0, {}),                              # class A only
+    ((200000, 50, 40), 300_000, 0.0, {}),                            # tiny segments, empty leading values
+])
+def test_middle_mode_counting_path_bit_exact(oracle, monkeypatch, shape, nnz, zipf, env):
+    """k == 1 (the paper's middle-mode protocol) through the segmented counting path
+    (tk_midmode.cu): class-A warp sorts, class-B counting tiles with the warp token ring and the
+    bucket folds -- bit-exact against the oracle, with the class thresholds shrunk to put most
+    rows through class B."""
+    import paper_2510_01495_b200 as tk
+    for kk, vv in env.items():
+        monkeypatch.setenv(kk, vv)
+    s, v = oracle.gen_coo(shape, nnz, zipf_s=zipf, normal_vals=True, seed=17)
+    x = oracle.gen_uniform(shape[1], 5)
+    es, ev, _ = oracle.ttv_raw(s, v, shape, x, 1)
+    gs, gv, gsh = tk.kernels().ttv_raw(s, v, shape, x, 1)
+    assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes() and len(ev) > 0
+
+
+def test_middle_mode_zero_groups_errors_and_declines(oracle):
+    """Exact-zero groups are removed (compaction), an out-of-range contracted index raises
+    DimensionError, garbage kept indices and an unsorted leading column decline to the general
+    paths -- all matching the oracle."""
+    import paper_2510_01495_b200 as tk
+    from paper_2510_01495_b200 import errors
+    K = tk.kernels()
+    shape = (20, 50, 30)
+    s, v = oracle.gen_coo(shape, 20000, seed=3)
+    v = v.copy()
+    # cancelling pairs: rows with equal (i0, i2) and adjacent i1 get +a / -a
+    key = s[:, 0] * 10**6 + s[:, 2]
+    order = np.lexsort((s[:, 1], key))
+    for a, b in zip(order[:-1:2], order[1::2]):
+        if key[a] == key[b] and a % 3 == 0:
+            v[b] = -v[a]
+    x = np.ones(shape[1])
+    es, ev, _ = oracle.ttv_raw(s, v, shape, x, 1)
+    gs, gv, _ = K.ttv_raw(s, v, shape, x, 1)
+    assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes()
+    bad = s.copy()
+    bad[777, 1] = shape[1]
+    with pytest.raises(errors.DimensionError):
+        K.ttv_raw(bad, v, shape, x, 1)
+    g = s.copy()
+    g[5, 2] = -3  # garbage kept index
+    es, ev, _ = oracle.ttv_raw(g, v, shape, x, 1)
+    gs, gv, _ = K.ttv_raw(g, v, shape, x, 1)
+    assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes()
+    perm = np.random.default_rng(1).permutation(len(v))  # leading column unsorted
+    es, ev, _ = oracle.ttv_raw(s[perm], v[perm], shape, x, 1)
+    gs, gv, _ = K.ttv_raw(s[perm], v[perm], shape, x, 1)
+    assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes()
+
+
+def test_cfg5_shape_middle_mode_1e8_rows_against_reference(oracle):
+    """The paper's protocol at scale: config-5 shape, 1e8 rows, k = 1 (contract the middle mode)
+    -- the counting path against the reference's own kernel on every host thread (shards cut at
+    leading-value changes), bit-exact."""
+    from paper_2510_01495_b200.device import DeviceCoo, uniform_vector
+    shape = (10**6, 10**5, 10**4)
+    t = DeviceCoo.generate(shape, 100_000_000, zipf_s=1.2, normal_vals=True, seed=12345)
+    x = uniform_vector(shape[1], 778)
+    u, os_d, ov_d = t.ttv(x, 1)
+    gs, gv = os_d[:u].cpu().numpy(), ov_d[:u].cpu().numpy()
+    subs, vals = t.to_host()
+    del t, os_d, ov_d
+    parts, _, kind = oracle.ttv_raw_threads(subs, vals, shape, x.cpu().numpy(), 1)
+    assert oracle.compare_parts(parts, gs, gv), kind
