@@ -355,6 +355,17 @@ def secondary_measurements(rank, steps, threads, with_cpu):
             return float("inf")
         return float(np.max(np.abs(got[nz] - exp[nz]) / np.abs(exp[nz]))) if nz.any() else 0.0
 
+    # the cold-read floor of each small config's byte count under the identical flush: a read-only
+    # stream kernel with dot's access pattern (tk_read_floor_f64_device)
+    floor_buf = torch.rand(134_283_264 // 8 + 2, dtype=torch.float64, device="cuda")
+    sink = torch.empty(148 * 8, dtype=torch.float64, device="cuda")
+    res["floor"] = {}
+    for name, nbytes in (("cfg1_16MB", 16_000_000), ("cfg3_47MB", 47_199_160), ("cfg2_134MB", 134_283_264)):
+        n = nbytes // 8 // 2 * 2
+        fms = kernel_ms(lambda: _lib.check(lib.tk_read_floor_f64_device(floor_buf.data_ptr(), n, sink.data_ptr(),
+                                                                         int(torch.cuda.current_stream().cuda_stream))))
+        res["floor"][name] = {"kernel_ms": fms, "GBps": nbytes / fms / 1e6}
+    del floor_buf, sink
     ops = synth.host_operands(1)
     x, y = torch.from_numpy(ops["x"]).cuda(), torch.from_numpy(ops["y"]).cuda()
     out = torch.empty(1, dtype=torch.float64, device="cuda")

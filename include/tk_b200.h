@@ -231,6 +231,11 @@ int tk_nccl_allgather_bytes(void* comm, const void* host_src, void* host_dst, in
 int tk_nccl_barrier(void* comm, void* stream);
 int tk_nccl_allreduce_sum_f64(void* comm, double* buf, int64_t n, void* stream);
 
+/* Measurement floor, not a reference kernel: a read-only stream of n doubles (device pointer,
+ * 16-byte aligned) with dot's load pattern and launch shape; its time under an L2 flush is the
+ * cold-read floor the small configs are judged against (tk_last_kernel_ms). */
+int tk_read_floor_f64_device(const double* p, int64_t n, double* sink, void* stream);
+
 /* ---- timing helper ----------------------------------------------------------------------- */
 /* Device milliseconds between two points on a stream (cudaEvent pair). */
 int tk_timer_start(void* stream);

@@ -78,6 +78,7 @@ SIGNATURES = {
     "tk_nccl_allgather_bytes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
     "tk_nccl_barrier": (ctypes.c_int, [_vp, _vp]),
     "tk_nccl_allreduce_sum_f64": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+    "tk_read_floor_f64_device": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp]),
     "tk_timer_start": (ctypes.c_int, [_vp]),
     "tk_timer_stop": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "tk_release": (ctypes.c_int, []),

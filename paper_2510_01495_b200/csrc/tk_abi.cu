@@ -219,6 +219,14 @@ int tk_dot_f64_host(const double* x, const double* y, int64_t n, double* out) {
   return TK_OK;
 }
 
+int tk_read_floor_f64_device(const double* p, int64_t n, double* sink, void* stream) {
+  if (n < 0 || (!p && n > 0) || !sink) return fail(TK_EARG, "read_floor: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = read_floor_device(p, n, sink, st)) return rc;
+  TK_CUDA(cudaStreamSynchronize(st));
+  return TK_OK;
+}
+
 int tk_matvec_f64_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, void* stream) {
   if (rows < 0 || cols < 0) return fail(TK_EARG, "matvec: negative shape");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -188,6 +188,39 @@ int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStr
   return TK_OK;
 }
 
+// Measurement floor (not a reference kernel): read n doubles with the dot kernel's access pattern
+// and launch shape -- every 16-byte load of the call in flight at once, a per-thread sum, one store
+// per CTA, no cross-CTA combine.  Timed under the same L2 flush as dot / matvec / the small TTV,
+// it is the cold-read time of those byte counts on this GPU (bench.py secondary "floor").
+__global__ void __launch_bounds__(kDotThreads) read_floor_kernel(const double2* __restrict__ p, long long n2,
+                                                                 double* __restrict__ sink) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (long long i = tid; i < n2; i += kDotUnroll * stride) {
+    double2 a[kDotUnroll];
+#pragma unroll
+    for (int u = 0; u < kDotUnroll; ++u) a[u] = i + u * stride < n2 ? __ldcs(p + i + u * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kDotUnroll; ++u) acc = __dadd_rn(acc, __dadd_rn(a[u].x, a[u].y));
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc == 1.2345e300) sink[blockIdx.x] = acc;  // keeps the loads alive
+}
+
+int read_floor_device(const double* p, int64_t n, double* sink, cudaStream_t st) {
+  if (n < 2) return TK_OK;
+  const long long n2 = n >> 1;
+  const long long want = (n2 + (long long)kDotThreads * kDotUnroll - 1) / ((long long)kDotThreads * kDotUnroll);
+  const int nblk = (int)std::max(1LL, std::min(want, (long long)num_sms() * 8));
+  ktimer_begin(st);
+  read_floor_kernel<<<nblk, kDotThreads, 0, st>>>(reinterpret_cast<const double2*>(p), n2, sink);
+  ktimer_end(st);
+  count_launch();
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
 int matvec_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, cudaStream_t st) {
   if (rows == 0) return TK_OK;
   const int vec2 = al16(a) && al16(x) && (cols % 2 == 0);

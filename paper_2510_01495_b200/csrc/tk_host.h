@@ -125,6 +125,7 @@ bool pack_rows(const RowPack& p, const int64_t* subs, const double* vals, int64_
 int unpack_rows(const RowPack& p, int64_t n, const uint64_t* packed, int64_t* soa, int64_t pitch, cudaStream_t st);
 
 int dot_device(const double* x, const double* y, int64_t n, double* out, cudaStream_t st);
+int read_floor_device(const double* p, int64_t n, double* sink, cudaStream_t st);
 int matvec_device(const double* a, int64_t rows, int64_t cols, const double* x, double* y, cudaStream_t st);
 
 }  // namespace tk

@@ -14,6 +14,7 @@
 //     PCIe bytes of the reference layout's 32 B per nonzero; the device unpacks into SoA columns.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -49,7 +50,7 @@ class HostPool {
       n_ = n;
       next_.store(0);
       pending_ = n;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     work();
@@ -73,10 +74,19 @@ class HostPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
-      {
+      // spin briefly before sleeping: a staged copy issues its chunk copies back to back, and a
+      // condition-variable wake-up costs tens of microseconds
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(200)) {
+      }
+      if (gen_.load(std::memory_order_acquire) == seen) {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);  // job_ / n_ of the new generation are published
+        seen = gen_.load(std::memory_order_acquire);
       }
       work();
     }
@@ -88,7 +98,7 @@ class HostPool {
   const std::function<void(int)>* job_ = nullptr;
   int n_ = 0, pending_ = 0, size_ = 1;
   std::atomic<int> next_{0};
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};
 };
 
 thread_local bool HostPool::in_job_ = false;
@@ -99,7 +109,8 @@ HostPool& pool() {
 }
 
 constexpr size_t kDirectBytes = 1u << 20;   // below this a pageable copy goes straight to the driver
-constexpr size_t kChunkBytes = 32u << 20;   // generic staged-copy chunk
+constexpr size_t kChunkBytes = 32u << 20;   // generic staged-copy chunk (largest)
+constexpr size_t kMinChunkBytes = 2u << 20;  // smallest chunk: the host copy of chunk i+1 overlaps the DMA of i
 
 struct Arena {  // per-device pinned staging, two halves used alternately
   std::mutex mu;
@@ -139,11 +150,11 @@ int host_threads() { return pool().size(); }
 void parallel_for(int n, const std::function<void(int)>& fn) { pool().run(n, fn); }
 
 void pmemcpy(void* dst, const void* src, size_t bytes) {
-  if (bytes < (4u << 20)) {
+  if (bytes < (512u << 10)) {
     memcpy(dst, src, bytes);
     return;
   }
-  const int parts = (int)std::min<size_t>(pool().size(), bytes / (1u << 20));
+  const int parts = (int)std::min<size_t>(pool().size(), bytes / (256u << 10));
   const size_t step = ((bytes + parts - 1) / parts + 63) & ~size_t(63);
   pool().run(parts, [&](int i) {
     const size_t a = std::min(bytes, (size_t)i * step), b = std::min(bytes, a + step);
@@ -169,7 +180,7 @@ int h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   Arena& a = arena(0);
   std::lock_guard<std::mutex> lk(a.mu);
   if (int rc = a.ensure(std::max(a.half, std::min(bytes, kChunkBytes)))) return rc;
-  const size_t chunk = std::min(a.half, std::max(kChunkBytes, bytes / 8));
+  const size_t chunk = std::min(a.half, std::max(kMinChunkBytes, std::min(kChunkBytes, bytes / 8)));
   int b = 0;
   for (size_t off = 0; off < bytes; off += chunk, b ^= 1) {
     const size_t n = std::min(chunk, bytes - off);
@@ -191,7 +202,7 @@ int d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   Arena& a = arena(1);
   std::lock_guard<std::mutex> lk(a.mu);
   if (int rc = a.ensure(std::max(a.half, std::min(bytes, kChunkBytes)))) return rc;
-  const size_t chunk = std::min(a.half, std::max(kChunkBytes, bytes / 8));
+  const size_t chunk = std::min(a.half, std::max(kMinChunkBytes, std::min(kChunkBytes, bytes / 8)));
   const size_t nch = (bytes + chunk - 1) / chunk;
   auto issue = [&](size_t i) -> int {
     const size_t off = i * chunk, n = std::min(chunk, bytes - off);
