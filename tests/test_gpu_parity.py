@@ -4,6 +4,8 @@ in-group folds, the reference's exact operation order); dot / matvec / dense
 multi-vector TTV within 1e-12 relative (north-star tolerance, written per test)."""
 
 import hashlib
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -255,15 +257,26 @@ def test_unique_rows_accumulate_matches_reference_pykernels_semantics(oracle):
         first[1:] = (ks[1:] != ks[:-1]).any(axis=1)
         assert np.array_equal(u, ks[first])
         exp = []
-        for i in np.flatnonzero(first):
+        for i in np.flatnonzero(first):  # the reference: acc = 0.0, then every weight in row order
             j = i
-            acc = w[order[i]]
-            j += 1
-            while j < n and not first[j]:
+            acc = 0.0
+            while j < n and (j == i or not first[j]):
                 acc += w[order[j]]
                 j += 1
             exp.append(acc)
         assert np.asarray(exp).tobytes() == s.tobytes()
+    # all-(-0.0) groups: the reference's fold from +0.0 gives +0.0
+    u, s = tk.unique_rows_accumulate([[1], [1], [2], [3], [3]], [-0.0, -0.0, -0.0, 5.0, -5.0])
+    assert u.tolist() == [[1], [2], [3]]
+    assert np.asarray([0.0, 0.0, 0.0]).tobytes() == s.tobytes()
+    if os.path.isdir(os.path.join(oracle.REF_DIR, "tenkern")):
+        sys.path.insert(0, oracle.REF_DIR)
+        from tenkern import _pykernels
+        for keys, w in (([[1], [1], [2]], [-0.0, -0.0, 0.5]), (rng.integers(0, 3, size=(200, 2)), rng.standard_normal(200))):
+            ru, rs = _pykernels.unique_rows_accumulate(np.asarray(keys, dtype=np.int64), np.asarray(w, dtype=np.float64))
+            gu, gs = tk.unique_rows_accumulate(keys, w)
+            assert np.asarray(ru).tolist() == gu.tolist()
+            assert np.asarray(rs, dtype=np.float64).tobytes() == gs.tobytes()
 
 
 def test_timed_entry_points(K):
