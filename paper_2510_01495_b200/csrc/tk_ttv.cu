@@ -696,7 +696,11 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
     p.prof = prof.as<unsigned long long>();
   }
 #endif
-  p.lag = std::min<long long>(TK_TILE_LAG, ntiles);
+  {  // TK_TILE_LAG_RT: run-time override of the count-to-fold lag (experiments)
+    const char* e = getenv("TK_TILE_LAG_RT");
+    const long long lag = e ? std::max(1LL, atoll(e)) : (long long)TK_TILE_LAG;
+    p.lag = std::min<long long>(lag, ntiles);
+  }
   p.ntiles = ntiles;
   p.out_v2 = p.out_nk == 2 && aligned16(p.out_subs);
   const char* mp = getenv("TK_TILE_MULTIPASS");  // tests force the fallback with "1"
@@ -755,6 +759,9 @@ int launch_stream(SegParams& p, cudaStream_t st, Counters* host_ctr) {
     case 1: return launch_stream_t<SRC, 1>(p, st, host_ctr);
     case 2: return launch_stream_t<SRC, 2>(p, st, host_ctr);
     case 3: return launch_stream_t<SRC, 3>(p, st, host_ctr);
+    case 4: return launch_stream_t<SRC, 4>(p, st, host_ctr);  // static key arrays up to order 7:
+    case 5: return launch_stream_t<SRC, 5>(p, st, host_ctr);  // the any-order instance keeps
+    case 6: return launch_stream_t<SRC, 6>(p, st, host_ctr);  // kMaxKeep-sized arrays in local memory
     default: return launch_stream_t<SRC, 0>(p, st, host_ctr);
   }
 }
