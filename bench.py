@@ -612,7 +612,7 @@ def run_ours(args):
             traffic = tj.get("dram_bytes_per_launch")
 
     # ---- host copies of the tensor and of the GPU result (outside every timed region) ----
-    need_host = rank == 0 and world == 1 and not (args.no_cpu and args.no_e2e)
+    need_host = (world == 1 and not (args.no_cpu and args.no_e2e)) or (world > 1 and not args.no_e2e)
     subs_h = vals_h = None
     if need_host:
         subs_h, vals_h = host_tensor(t)
@@ -628,7 +628,7 @@ def run_ours(args):
     #      caller holds (H2D of the tensor, TTV, D2H of the result, host reassembly) ----
     e2e = None
     if not args.no_e2e and subs_h is not None:
-        e2e = run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals)
+        e2e = run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals, world, nnz_total)
 
     parity = None
     cpu_leg = None
@@ -686,7 +686,7 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals):
+def run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals, world=1, nnz_total=None):
     """The reference caller's call: ``kernels().ttv_raw(subs, vals, shape, x, k)`` with the
     pageable, read-only numpy arrays a SparseCooTensor holds (pkg/src/tenkern/sparse.py:101-107),
     timed from the host (copies in and out, GPU work and the fresh output arrays inside)."""
@@ -707,8 +707,8 @@ def run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals):
         native.append(_lib.load().tk_last_call_seconds())
         u = len(res[1])
         del res
-    el = float(np.mean(ts))
-    n = subs_h.shape[0]
+    el = max_over_ranks(float(np.mean(ts)), world)  # N > 1: every rank's drop-in call on its shard
+    n = subs_h.shape[0] if world == 1 else int(nnz_total)
     return {"value": n / el, "unit": "nnz/s", "h2d_bytes_per_step": int(n * 32 + 8 * xh.shape[0]),
             "h2d_wire_bytes_per_step": int(n * 16 + 8 * xh.shape[0]),  # packed rows (RowPack) + values
             "d2h_bytes_per_step": int(u * 24), "ms_per_step": el * 1e3, "native_ms_per_step": 1e3 * float(np.mean(native)),

@@ -47,7 +47,10 @@ namespace {
 
 constexpr int kMidThreads = 256;       // every kernel with a token ring: 8 warps
 constexpr int kMidWarps = kMidThreads / 32;
-constexpr int kWin = 2048;             // class A: segments of at most kWin rows; windows of kWin rows
+#ifndef TK_MID_WIN
+#define TK_MID_WIN 2048
+#endif
+constexpr int kWin = TK_MID_WIN;             // class A: segments of at most kWin rows; windows of kWin rows
 constexpr int kBufRows = 2 * kWin;     // rows of one class-A window (segments starting in it)
 constexpr long long kMidMaxR = 16384;  // suffix key S < 2^14
 constexpr int kChunkTiles = 32;        // column scan: tiles per chunk
