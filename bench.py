@@ -712,6 +712,7 @@ def run_e2e(subs_h, vals_h, shape, xh, k, args, gpu_subs, gpu_vals, world=1, nnz
     return {"value": n / el, "unit": "nnz/s", "h2d_bytes_per_step": int(n * 32 + 8 * xh.shape[0]),
             "h2d_wire_bytes_per_step": int(n * 16 + 8 * xh.shape[0]),  # packed rows (RowPack) + values
             "d2h_bytes_per_step": int(u * 24), "ms_per_step": el * 1e3, "native_ms_per_step": 1e3 * float(np.mean(native)),
+            "ms_steps": [round(v * 1e3, 1) for v in ts],
             "steps": steps, "result_matches_device_path": same,
             "path": "kernels().ttv_raw(subs, vals, shape, x, k) on pageable read-only numpy arrays "
                     "(the reference's kernel-module call) -> tk_ttv_f64_host: rows packed to 64-bit words by "

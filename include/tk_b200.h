@@ -248,8 +248,16 @@ double tk_last_kernel_ms(void);
 /* Number of kernels this library has launched in this process (instrumentation). */
 long long tk_launch_count(void);
 
-/* Release cached device memory (pool trim) and pinned scratch. */
+/* Release cached device memory (pool trim), pinned scratch and cached result blocks. */
 int tk_release(void);
+
+/* Pinned host blocks for results of the host-buffer calls, cached across calls: a caller that
+ * allocates its output arrays here (the Python module does for results >= 64 MB) gets the D2H
+ * straight into them.  *out = NULL (status TK_OK) when the cache cap (a quarter of host RAM,
+ * env TK_HOST_POOL_MB) would be exceeded -- allocate ordinary memory then.  tk_host_free returns
+ * the block to the cache (TK_EARG for a pointer that is not a live block). */
+int tk_host_alloc(size_t bytes, void** out);
+int tk_host_free(void* p);
 
 #ifdef __cplusplus
 }

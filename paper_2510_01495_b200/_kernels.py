@@ -37,6 +37,39 @@ def _f64(a, ndim):
     return arr
 
 
+class _PinnedBlock:
+    """A cached pinned result block (tk_host_alloc); numpy views keep it alive, and it goes back
+    to the library's cache when the last view is dropped."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr = ptr
+        self.__array_interface__ = {"data": (ptr, False), "shape": (nbytes,), "typestr": "|u1", "version": 3}
+
+    def __del__(self):
+        try:
+            _lib.load().tk_host_free(self.ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_POOLED_RESULT_BYTES = 64 << 20
+
+
+def _result_arrays(rows: int, cols: int):
+    """(subs[rows, cols] int64, vals[rows] float64) for a host-call result.  Large results come
+    from the library's pinned cache, so the device writes them directly; small ones (and any
+    request past the cache cap) are ordinary owned arrays."""
+    nbytes = rows * (cols + 1) * 8
+    if nbytes >= _POOLED_RESULT_BYTES:
+        p = ctypes.c_void_p()
+        _lib.check(_lib.load().tk_host_alloc(nbytes, ctypes.byref(p)))
+        if p.value:
+            buf = np.asarray(_PinnedBlock(p.value, nbytes))
+            cut = rows * cols * 8
+            return buf[:cut].view(np.int64).reshape(rows, cols), buf[cut:].view(np.float64), True
+    return np.empty((rows, cols), dtype=np.int64), np.empty(rows, dtype=np.float64), False
+
+
 def _check_dot(x, y):
     if x.shape[0] != y.shape[0]:
         raise DimensionError(f"dot: operand lengths differ: {x.shape[0]} vs {y.shape[0]}")
@@ -94,14 +127,15 @@ def _ttv_host(subs, vals, shape, x, k):
         raise DimensionError(f"ttv: subs of shape {sv.shape} and {vv.shape[0]} values do not match order {d}")
     nnz = sv.shape[0]
     new_shape = tuple(shape[m] for m in range(d) if m != k)
-    out_subs = np.empty((max(nnz, 1), d - 1), dtype=np.int64)
-    out_vals = np.empty(max(nnz, 1), dtype=np.float64)
+    out_subs, out_vals, pooled = _result_arrays(max(nnz, 1), d - 1)
     u = ctypes.c_int64(0)
     shp = _lib.i64_array(shape)
     _lib.check(_lib.load().tk_ttv_f64_host(d, shp, nnz, sv.ctypes.data, vv.ctypes.data, xv.ctypes.data,
                                             xv.shape[0], k, out_subs.ctypes.data, out_vals.ctypes.data,
                                             ctypes.byref(u)))
     n = u.value
+    if pooled:  # exact-size views of the cached pinned block (released when the caller drops them)
+        return out_subs[:n], out_vals[:n], new_shape
     # fresh, owned, exact-size outputs like the reference's copy-out (pyx:367), without a second
     # host copy: the capacity-sized buffers are shrunk in place (realloc; pages past u were never
     # touched, so they were never committed)

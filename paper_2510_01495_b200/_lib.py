@@ -82,6 +82,8 @@ SIGNATURES = {
     "tk_timer_start": (ctypes.c_int, [_vp]),
     "tk_timer_stop": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "tk_release": (ctypes.c_int, []),
+    "tk_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "tk_host_free": (ctypes.c_int, [_vp]),
     "tk_last_kernel_ms": (ctypes.c_double, []),
     "tk_launch_count": (ctypes.c_longlong, []),
 }

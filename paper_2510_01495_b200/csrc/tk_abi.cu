@@ -334,8 +334,32 @@ PipeStage& pipe_stage() {
 // when every index fits its dimension, else the raw int64 rows) with the thread pool while the
 // DMA of chunk i runs, and copies chunk i-1's result out of its staging half in parallel.
 // Declines (kPipeDeclined) if the input is not in kept-key order -- the one-shot path then sorts.
+// TK_PIPE_TIMING=1: where the host time of one pipelined call goes (stderr; diagnostics only).
+struct PipeTimes {
+  using clk = std::chrono::steady_clock;
+  bool on = getenv("TK_PIPE_TIMING") != nullptr;
+  double t[6] = {0, 0, 0, 0, 0, 0};  // wait_in, pack, wait_free, copy_out, final_sync, total
+  clk::time_point t0 = clk::now();
+  struct Span {
+    PipeTimes* p;
+    int i;
+    clk::time_point s = clk::now();
+    ~Span() {
+      if (p->on) p->t[i] += std::chrono::duration<double>(clk::now() - s).count();
+    }
+  };
+  Span span(int i) { return Span{this, i}; }
+  ~PipeTimes() {
+    if (!on) return;
+    t[5] = std::chrono::duration<double>(clk::now() - t0).count();
+    fprintf(stderr, "[tk pipe] wait_in %.1f pack %.1f wait_free %.1f copy_out %.1f final_sync %.1f total %.1f ms\n",
+            t[0] * 1e3, t[1] * 1e3, t[2] * 1e3, t[3] * 1e3, t[4] * 1e3, t[5] * 1e3);
+  }
+};
+
 int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* subs, const double* vals,
                        const double* x, int64_t nx, int64_t* out_subs, double* out_vals, int64_t* out_nnz) {
+  PipeTimes pt;
   const int nk = d - 1;
   std::vector<int64_t> cut{0};
   while (cut.back() < nnz) {
@@ -404,7 +428,11 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
       TK_CUDA(cudaMemcpyAsync(b_aos[b].get(), subs + cut[i] * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, si));
       TK_CUDA(cudaMemcpyAsync(b_vals[b].get(), vals + cut[i], (size_t)n * 8, cudaMemcpyHostToDevice, si));
     } else {
-      TK_CUDA(cudaEventSynchronize(ev_in[b]));  // the DMA that last read this staging half is done
+      {
+        auto sp = pt.span(0);
+        TK_CUDA(cudaEventSynchronize(ev_in[b]));  // the DMA that last read this staging half is done
+      }
+      auto sp = pt.span(1);
       char* stg = ps->in + (size_t)b * ps->in_half;
       double* sv = reinterpret_cast<double*>(stg + (size_t)rows * d * 8);
       packed[b] = packable && pack_rows(rp, subs + cut[i] * d, vals + cut[i], n, reinterpret_cast<uint64_t*>(stg), sv);
@@ -421,7 +449,11 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
   std::vector<int64_t> offs(nchunk + 1, 0), us(nchunk, 0);
   auto copy_out_host = [&](int i) -> int {  // pageable outputs: staging half -> caller, in parallel
     const int b = i & 1;
-    TK_CUDA(cudaEventSynchronize(ev_free[b]));
+    {
+      auto sp = pt.span(2);
+      TK_CUDA(cudaEventSynchronize(ev_free[b]));
+    }
+    auto sp = pt.span(3);
     const int64_t u = us[i];
     char* stg = ps->out + (size_t)b * ps->out_half;
     pmemcpy(out_subs + offs[i] * nk, stg, (size_t)u * nk * 8);
@@ -468,8 +500,11 @@ int ttv_host_pipelined(int d, const int64_t* shape, int64_t nnz, const int64_t* 
     if (!pin_out && i >= 1)
       if (int rc = copy_out_host(i - 1)) return rc;
   }
-  TK_CUDA(cudaStreamSynchronize(so));
-  TK_CUDA(cudaStreamSynchronize(sc));
+  {
+    auto sp = pt.span(4);
+    TK_CUDA(cudaStreamSynchronize(so));
+    TK_CUDA(cudaStreamSynchronize(sc));
+  }
   if (!pin_out && nchunk >= 1)
     if (int rc = copy_out_host(nchunk - 1)) return rc;
   *out_nnz = offs[nchunk];
@@ -892,6 +927,18 @@ int tk_release(void) {
   if (g_pinned) cudaFreeHost(g_pinned);
   g_pinned = nullptr;
   g_pinned_bytes = 0;
+  host_result_trim();
+  return TK_OK;
+}
+
+int tk_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(TK_EARG, "host_alloc: null out");
+  *out = host_result_alloc(bytes);
+  return TK_OK;
+}
+
+int tk_host_free(void* p) {
+  if (p && !host_result_free(p)) return fail(TK_EARG, "host_free: not a block from tk_host_alloc");
   return TK_OK;
 }
 

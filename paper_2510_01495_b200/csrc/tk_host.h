@@ -106,6 +106,11 @@ int host_threads();
 void parallel_for(int n, const std::function<void(int)>& fn);  // persistent host thread pool
 void pmemcpy(void* dst, const void* src, size_t bytes);          // parallel host memcpy
 bool host_is_pinned(const void* p);
+// cached pinned result blocks (capped at a quarter of host RAM, TK_HOST_POOL_MB overrides);
+// alloc returns nullptr when the cap is reached
+void* host_result_alloc(size_t bytes);
+bool host_result_free(void* p);
+void host_result_trim();
 // H2D / D2H of caller host memory: pinned -> direct DMA; pageable -> chunked through a per-device
 // pinned arena (parallel host copy of chunk i+1 overlapping the DMA of chunk i).  h2d is
 // stream-ordered (the source may be reused on return); d2h returns with the data on the host.

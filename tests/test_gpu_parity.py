@@ -415,6 +415,46 @@ def test_host_pipeline_pinned_and_unpackable_chunks(oracle):
     assert s2.tobytes() == es2.tobytes() and v2.tobytes() == ev2.tobytes()
 
 
+def test_pooled_pinned_results_do_not_alias(oracle, tmp_path):
+    """Results >= 64 MB come from the library's cached pinned blocks (the D2H writes the caller's
+    arrays directly).  A block stays live while any view of it does: a second call made while the
+    first result is held must get different memory; a dropped result's block is reused.  With the
+    cache disabled (TK_HOST_POOL_MB=0) the results are ordinary owned arrays, bit-identical."""
+    import subprocess
+    import paper_2510_01495_b200 as tk
+    K = tk.kernels()
+    shape = (300000, 2000, 3000)
+    subs, vals = oracle.gen_coo(shape, 20_000_000, zipf_s=1.1, normal_vals=True, seed=41)
+    x2 = oracle.gen_uniform(shape[2], 5)
+    x0 = oracle.gen_uniform(shape[0], 6)
+    es, ev, _ = oracle.ttv_raw(subs, vals, shape, x2, 2)
+    r1 = K.ttv_raw(subs, vals, shape, x2, 2)  # pipelined host path
+    assert not r1[1].flags.owndata and r1[1].flags.writeable and r1[0].flags.c_contiguous
+    assert r1[0].tobytes() == es.tobytes() and r1[1].tobytes() == ev.tobytes()
+    r2 = K.ttv_raw(subs, vals, shape, x2, 2)
+    assert not np.shares_memory(r1[1], r2[1]) and not np.shares_memory(r1[0], r2[0])
+    assert r1[1].tobytes() == ev.tobytes() and r2[1].tobytes() == ev.tobytes()
+    r2[1][:] = 0.0  # the caller owns its result
+    assert r1[1].tobytes() == ev.tobytes()
+    del r1, r2
+    fs, fv, _ = oracle.ttv_raw(subs, vals, shape, x0, 0)
+    r3 = K.ttv_raw(subs, vals, shape, x0, 0)  # one-shot host path, direct D2H into the block
+    assert r3[0].tobytes() == fs.tobytes() and r3[1].tobytes() == fv.tobytes()
+    np.save(tmp_path / "s.npy", subs)
+    np.save(tmp_path / "v.npy", vals)
+    np.save(tmp_path / "x.npy", x2)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[2]); import paper_2510_01495_b200 as tk; "
+        "p = sys.argv[1]; s = np.load(p + '/s.npy'); v = np.load(p + '/v.npy'); x = np.load(p + '/x.npy'); "
+        f"r = tk.kernels().ttv_raw(s, v, {shape!r}, x, 2); assert r[0].flags.owndata and r[1].flags.owndata; "
+        "np.save(p + '/rs.npy', r[0]); np.save(p + '/rv.npy', r[1])")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TK_HOST_POOL_MB="0")
+    subprocess.run([sys.executable, "-c", code, str(tmp_path), repo], env=env, check=True, timeout=600)
+    assert np.load(tmp_path / "rs.npy").tobytes() == es.tobytes()
+    assert np.load(tmp_path / "rv.npy").tobytes() == ev.tobytes()
+
+
 def _canonical_coo(shape, nnz, seed):
     """Distinct uniform coordinates in canonical (lexicographic) order, positive values."""
     rng = np.random.default_rng(seed)
