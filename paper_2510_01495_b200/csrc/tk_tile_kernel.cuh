@@ -68,7 +68,17 @@ constexpr int kTileWarps = kTileThreads / 32;
 #ifndef TK_SPILL_W0FIRST
 #define TK_SPILL_W0FIRST 0  // with an open group, warp 0 skips the striped folds (measured slower)
 #endif
-constexpr int kSpillSlots = TK_SPILL_SLOTS;  // 128-row chunks of the spill ring (in the 6.4 KB subk column)
+constexpr int kSpillSlots = TK_SPILL_SLOTS;
+// The count's key loads stream through once (the stage re-reads them by TMA, into shared memory):
+// cache them in L2 only, so L1 keeps the gathered vector x.
+#ifndef TK_CNT_CG
+#define TK_CNT_CG 1
+#endif
+#if TK_CNT_CG
+#define TK_CNT_LD(ptr) __ldcg(ptr)
+#else
+#define TK_CNT_LD(ptr) (*(ptr))
+#endif  // 128-row chunks of the spill ring (in the 6.4 KB subk column)
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
@@ -320,9 +330,9 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
 #pragma unroll
       for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int c = 0; c < NKV; ++c) v[b][c] = reinterpret_cast<const longlong2*>(p.key[c] + r0 + 64 * b)[lane];
+        for (int c = 0; c < NKV; ++c) v[b][c] = TK_CNT_LD(reinterpret_cast<const longlong2*>(p.key[c] + r0 + 64 * b) + lane);
 #pragma unroll
-      for (int c = 0; c < NKV; ++c) edge[c] = (lane == 31 && r0 > 0) ? p.key[c][r0 - 1] : 0;
+      for (int c = 0; c < NKV; ++c) edge[c] = (lane == 31 && r0 > 0) ? TK_CNT_LD(p.key[c] + r0 - 1) : 0;
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         bool ne0 = false, ne1 = false;
@@ -346,7 +356,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
-        cur[j][c] = ok ? p.key[c][cstart + rl] : 0;
+        cur[j][c] = ok ? TK_CNT_LD(p.key[c] + cstart + rl) : 0;
       }
     }
     {
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(kTileThreads, TK_TILE_MINB) ttv_tile_kernel(Se
 #pragma unroll
       for (int c = 0; c < NKR; ++c) {
         if (NK == 0 && c >= nk) break;
-        edge[c] = ok ? p.key[c][cstart + wrow0 - 1] : 0;
+        edge[c] = ok ? TK_CNT_LD(p.key[c] + cstart + wrow0 - 1) : 0;
       }
     }
 #pragma unroll

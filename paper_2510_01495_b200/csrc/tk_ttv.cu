@@ -677,7 +677,27 @@ int launch_stream_t(SegParams& p, cudaStream_t st, Counters* host_ctr) {
   const int ncol = nk + 1 + (SRC == kSrcRaw ? 1 : 0);
   const size_t smem = tile_total_smem<SRC, TILE, HALO>(ncol, nk);
   auto kern = ttv_tile_kernel<SRC, NK, TILE, HALO>;
-  set_smem_once(kern, smem);
+  // Raw source: shared memory for 7 CTAs per SM, not 8 -- the unified L1 keeps the rest (60 KB vs
+  // 28 KB on sm_100), enough for the hot part of the gathered vector x: config 5 3.33 -> 3.24 ms
+  // (5 CTAs: 3.80 ms).  Precomputed-w sources gather nothing and keep every CTA.
+  // TK_TILE_CARVEOUT=<percent> overrides (diagnostics).
+  static const int tile_carveout = [smem] {
+    if (const char* e = getenv("TK_TILE_CARVEOUT")) return std::max(0, std::min(100, atoi(e)));
+    if (SRC != kSrcRaw) return 100;
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (per_sm <= 0) return 100;
+    return (int)std::min<size_t>(100, (100 * 7 * (smem + 1024) + per_sm - 1) / per_sm);
+  }();
+  set_smem_once(kern, smem, tile_carveout);
+  if (getenv("TK_TILE_CARVEOUT")) {
+    static bool once = false;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem);
+    if (!once) fprintf(stderr, "[tk tile] carveout %d%%: %d CTAs/SM, %zu B smem each\n", tile_carveout, per_sm, smem);
+    once = true;
+  }
   const long long ntiles = (p.n + TILE - 1) / TILE;
   const size_t status_b = ((size_t)ntiles * 8 + 255) & ~size_t(255);
   DevBuf scratch;
