@@ -18,3 +18,13 @@ starts = torch.cumsum(counts, 0) - counts
 ends = starts + counts
 span = (starts // tile) != ((ends - 1) // tile)
 print(f"  groups crossing a {tile}-row tile edge: {int(span.sum())} rows: {float(c[span].sum())/nnz*100:.2f}%")
+# rows a tile's open group holds past its stage (tile + halo): what a second-pass chain kernel would re-read
+halo = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+stage_end = (starts // tile + 1) * tile + halo
+past = torch.clamp(ends - stage_end, min=0)
+m = past > 0
+print(f"  open groups past a {tile}+{halo} stage: {int(m.sum())}  rows past the stage: {float(past.sum())/nnz*100:.2f}%  "
+      f"in-stage rows of those groups: {float((c[m]-past[m].double()).sum())/nnz*100:.2f}%")
+for th in (64, 128, 256, 512):
+    big = counts > th
+    print(f"  groups > {th} rows: {int(big.sum())}, rows {float(c[big].sum())/nnz*100:.2f}%")
