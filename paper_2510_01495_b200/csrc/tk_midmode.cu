@@ -47,14 +47,13 @@ namespace {
 
 constexpr int kMidThreads = 256;       // every kernel with a token ring: 8 warps
 constexpr int kMidWarps = kMidThreads / 32;
-#ifndef TK_MID_WIN
-#define TK_MID_WIN 2048
+#ifndef TK_MID_WARPMAX
+#define TK_MID_WARPMAX 512
 #endif
-constexpr int kWin = TK_MID_WIN;             // class A: segments of at most kWin rows; windows of kWin rows
-constexpr int kBufRows = 2 * kWin;     // rows of one class-A window (segments starting in it)
+constexpr int kWarpMax = TK_MID_WARPMAX;  // class A: segments of at most kWarpMax rows, one warp each
 constexpr long long kMidMaxR = 16384;  // suffix key S < 2^14
 constexpr int kChunkTiles = 32;        // column scan: tiles per chunk
-constexpr long long kMedMax = 65536;   // class M: segments of kWin+1 .. kMedMax rows
+constexpr long long kMedMax = 65536;   // class M: segments of kWarpMax+1 .. kMedMax rows
 constexpr long long kTileRows = 262144;  // class B counting tile (long runs per bucket: full-sector writes)
 constexpr int kMedBigList = kMedMax / 24;  // class M: warp-folded buckets of one segment
 
@@ -89,10 +88,6 @@ struct MidParams {
   double* out_vals;
   const long long* out_base;       // n0 + 1: first output row of every segment
   long long* groups;               // n0: groups of every segment
-  int* ti0;                        // class A scratch by class-A row (abase[i0] + rank): leading value,
-  unsigned int* tkey;              //   S of the segment's rank-th group
-  double* tval;                    //   and its value
-  const long long* abase;          // n0 + 1: first class-A row of every segment (class A only)
   long long med_max;               // class M / class B boundary (rows)
   Counters* ctr;
 };
@@ -102,7 +97,7 @@ __device__ __forceinline__ long long suffix_key(const MidParams& p, long long r,
   const int ns = NS > 0 ? NS : p.ns;
   long long s = 0;
   for (int j = 0; j < ns; ++j) {
-    const long long v = __ldg(p.sc[j] + r);
+    const long long v = __ldcs(p.sc[j] + r);
     if ((unsigned long long)v >= (unsigned long long)p.sdim[j]) flags |= kFlagKeptOob;
     s = s * p.sdim[j] + v;
   }
@@ -117,13 +112,17 @@ __device__ __forceinline__ double row_w(const MidParams& p, long long r, unsigne
 }
 
 __device__ __forceinline__ void emit_group(const MidParams& p, long long g, long long i0, long long s, double v) {
+  p.out_vals[g] = v;
+  if (p.ns == 1) {  // (i0, S) is the output row: one 16-byte store
+    *reinterpret_cast<longlong2*>(p.out_subs + 2 * g) = make_longlong2(i0, s);
+    return;
+  }
   long long* o = p.out_subs + g * p.nk;
   o[0] = i0;
   for (int j = p.ns - 1; j >= 0; --j) {
     o[1 + j] = s % p.sdim[j];
     s /= p.sdim[j];
   }
-  p.out_vals[g] = v;
 }
 
 __device__ __forceinline__ void flush_counters(const MidParams& p, unsigned int flags, unsigned int zeros) {
@@ -135,60 +134,96 @@ __device__ __forceinline__ void flush_counters(const MidParams& p, unsigned int 
   }
 }
 
-// Serial left fold of src[0..n) (acc = src[0]; acc = __dadd_rn(acc, src[1]) ...) by one warp: the
-// lanes load 32-value chunks kRingChunks chunks ahead and park each in a per-warp shared ring just
-// before it is needed; lane 0 adds in order from the ring (16-byte shared loads).  Lane 0's result.
+// Serial left fold of src[0..n) by one warp: the lanes load 32-value chunks kRingChunks chunks ahead
+// and park two chunks per round in a per-warp shared ring just before they are needed; lane 0 adds
+// the 64 values in order from the ring (16-byte shared loads, unrolled: the chain runs at the
+// 8-cycle latency of a dependent DADD).  The accumulator starts at -0.0, the exact additive
+// identity under round-to-nearest, so the result has the bits of w[0] + w[1] + ... folded left to
+// right.  Lane 0's result.
 constexpr int kRingChunks = 8;
+
+__device__ __forceinline__ double fold_ring_rows(const double* c, int m, double acc) {
+  int j = 0;
+  for (; j + 16 <= m; j += 16) {
+    double2 pr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pr[q] = *reinterpret_cast<const double2*>(c + j + 2 * q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc = __dadd_rn(acc, pr[q].x);
+      acc = __dadd_rn(acc, pr[q].y);
+    }
+  }
+  for (; j < m; ++j) acc = __dadd_rn(acc, c[j]);
+  return acc;
+}
 
 __device__ __forceinline__ double warp_serial_fold(const double* __restrict__ src, long long n, double* ring) {
   const int lane = threadIdx.x & 31;
   double v[kRingChunks];
 #pragma unroll
-  for (int a = 0; a < kRingChunks; ++a) v[a] = a * 32 + lane < n ? src[a * 32 + lane] : 0.0;
-  double acc = 0.0;
+  for (int a = 0; a < kRingChunks; ++a) v[a] = a * 32 + lane < n ? __ldcs(src + a * 32 + lane) : 0.0;
+  double acc = -0.0;
   const long long nch = (n + 31) / 32;
-  for (long long k = 0; k < nch; ++k) {
-    const int a = (int)(k % kRingChunks);
-    double cur = 0.0;
+  for (long long k0 = 0; k0 < nch; k0 += kRingChunks) {
 #pragma unroll
-    for (int q = 0; q < kRingChunks; ++q)
-      if (q == a) {
-        cur = v[q];
-        const long long nx = (k + kRingChunks) * 32 + lane;
-        v[q] = nx < n ? src[nx] : 0.0;  // in flight while lane 0 adds
-      }
-    ring[a * 32 + lane] = cur;
-    __syncwarp();
-    if (lane == 0) {
-      const double* c = ring + a * 32;
-      const int m = (int)min(32LL, n - k * 32);
-      int j = 0;
-      if (k == 0) {
-        acc = c[0];
-        j = 1;
-        if (m > 1) {
-          acc = __dadd_rn(acc, c[1]);
-          j = 2;
-        }
-      }
-      for (; j + 2 <= m; j += 2) {
-        const double2 pr = *reinterpret_cast<const double2*>(c + j);
-        acc = __dadd_rn(acc, pr.x);
-        acc = __dadd_rn(acc, pr.y);
-      }
-      if (j < m) acc = __dadd_rn(acc, c[j]);
+    for (int a = 0; a < kRingChunks; a += 2) {  // static ring slots: chunk k lives in slot k % kRingChunks
+      const long long k = k0 + a;
+      if (k >= nch) break;  // warp-uniform
+      ring[a * 32 + lane] = v[a];
+      ring[(a + 1) * 32 + lane] = v[a + 1];
+      const long long nx = (k + kRingChunks) * 32 + lane;
+      v[a] = nx < n ? __ldcs(src + nx) : 0.0;  // in flight while lane 0 adds
+      v[a + 1] = nx + 32 < n ? __ldcs(src + nx + 32) : 0.0;
+      __syncwarp();
+      if (lane == 0) acc = fold_ring_rows(ring + a * 32, (int)min(64LL, n - k * 32), acc);
+      __syncwarp();
     }
-    __syncwarp();
   }
   return acc;
 }
 
+// Serial left fold of src[0..n) by one thread (buckets of kBigBucket..kHugeBucket rows, one per
+// lane): eight values in flight ahead of the dependent adds.
+__device__ __forceinline__ double lane_serial_fold(const double* __restrict__ src, unsigned int n) {
+  double acc = -0.0;
+  unsigned int j = 0;
+  if ((reinterpret_cast<unsigned long long>(src) & 8ull) && n > 0) acc = __dadd_rn(acc, src[j++]);  // 16-byte alignment
+  double2 cur[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    cur[q] = j + 2 * q + 2 <= n ? __ldcs(reinterpret_cast<const double2*>(src + j) + q) : make_double2(0.0, 0.0);
+  for (; j + 8 <= n; j += 8) {
+    double2 nxt[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      nxt[q] = j + 8 + 2 * q + 2 <= n ? __ldcs(reinterpret_cast<const double2*>(src + j + 8) + q) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc = __dadd_rn(acc, cur[q].x);
+      acc = __dadd_rn(acc, cur[q].y);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // the last 0..7 values: pairs already loaded, then an odd one
+    if (j + 2 <= n) {
+      acc = __dadd_rn(acc, cur[q].x);
+      acc = __dadd_rn(acc, cur[q].y);
+      j += 2;
+    }
+  }
+  if (j < n) acc = __dadd_rn(acc, src[j]);
+  return acc;
+}
+
 // ---- planning ---------------------------------------------------------------------------------
-// per segment: class-B flag, tile and chunk counts, class-M flag, class-A rows (all exclusive-scanned)
+// per segment: class-B flag, tile and chunk counts, class-M flag, class-A flag (all exclusive-scanned)
 __global__ void mid_classify_kernel(long long n0, const long long* __restrict__ off, long long tile_rows,
                                     long long med_max, long long* __restrict__ isb, long long* __restrict__ ntile,
                                     long long* __restrict__ nchunk, long long* __restrict__ ism,
-                                    long long* __restrict__ arows) {
+                                    long long* __restrict__ isa) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n0; i += (long long)gridDim.x * blockDim.x) {
     const long long L = off[i + 1] - off[i];
     const bool b = L > med_max;
@@ -196,19 +231,16 @@ __global__ void mid_classify_kernel(long long n0, const long long* __restrict__ 
     isb[i] = b;
     ntile[i] = nt;
     nchunk[i] = (nt + kChunkTiles - 1) / kChunkTiles;
-    ism[i] = L > kWin && !b;
-    arows[i] = (L >= 1 && L <= kWin) ? L : 0;
+    ism[i] = L > kWarpMax && !b;
+    isa[i] = L >= 1 && L <= kWarpMax;
   }
 }
 
-// class-B and class-M segment lists (ascending i0), the segment of every class-B tile / chunk, and
-// the first segment of every class-A window (a segment belongs to the window its first class-A
-// row falls in)
-__global__ void mid_lists_kernel(long long n0, const long long* __restrict__ off, const long long* __restrict__ bidx,
-                                 const long long* __restrict__ tbase, const long long* __restrict__ cbase,
-                                 const long long* __restrict__ midx, const long long* __restrict__ abase,
-                                 int* __restrict__ blist, int* __restrict__ tile_seg, int* __restrict__ chunk_seg,
-                                 int* __restrict__ mlist, int* __restrict__ wfirst) {
+// class-B, class-M and class-A segment lists (ascending i0) and the segment of every class-B tile / chunk
+__global__ void mid_lists_kernel(long long n0, const long long* __restrict__ bidx, const long long* __restrict__ tbase,
+                                 const long long* __restrict__ cbase, const long long* __restrict__ midx,
+                                 const long long* __restrict__ aidx, int* __restrict__ blist, int* __restrict__ tile_seg,
+                                 int* __restrict__ chunk_seg, int* __restrict__ mlist, int* __restrict__ alist) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n0; i += (long long)gridDim.x * blockDim.x) {
     if (bidx[i + 1] != bidx[i]) {
       blist[bidx[i]] = (int)i;
@@ -216,7 +248,7 @@ __global__ void mid_lists_kernel(long long n0, const long long* __restrict__ off
       for (long long c = cbase[i]; c < cbase[i + 1]; ++c) chunk_seg[c] = (int)i;
     }
     if (midx[i + 1] != midx[i]) mlist[midx[i]] = (int)i;
-    if (abase[i + 1] != abase[i]) atomicMin(&wfirst[abase[i] / kWin], (int)i);
+    if (aidx[i + 1] != aidx[i]) alist[aidx[i]] = (int)i;
   }
 }
 
@@ -224,7 +256,10 @@ __global__ void mid_lists_kernel(long long n0, const long long* __restrict__ off
 // w = vals * x[i1] stably to dst[cur[S]++] (token ring: the eight warps update the cursors in
 // turn, ranks inside a warp step from __match_any_sync).  The raw loads (S columns, i1, vals) are
 // issued kPipe steps ahead and the x gather one step ahead, so no instruction waits on a load
-// issued in the same step.
+// issued in the same step; the step loop is unrolled by kPipe so the look-ahead slots are
+// registers (a runtime slot index put them in local memory: 35% of the stall samples).  A warp's
+// turn is one shared load and one store by the first lane of every distinct S; the other lanes
+// take their bucket's base from that lane afterwards.
 constexpr int kPipe = 4;
 
 template <int NS>
@@ -238,8 +273,8 @@ __device__ __forceinline__ void stream_scatter(const MidParams& p, long long r0,
   auto load_raw = [&](long long r, long long& s, long long& i1, double& v) {
     if (r < r1) {
       s = suffix_key<NS>(p, r, flags);
-      i1 = __ldg(p.c1 + r);
-      v = __ldg(p.vals + r);
+      i1 = __ldcs(p.c1 + r);
+      v = __ldcs(p.vals + r);
     } else {
       s = -1 - lane;
       i1 = 0;
@@ -254,33 +289,29 @@ __device__ __forceinline__ void stream_scatter(const MidParams& p, long long r0,
 #pragma unroll
   for (int a = 0; a < kPipe; ++a) load_raw(r0 + a * kMidThreads + warp * 32 + lane, sq[a], iq[a], vq[a]);
   double xcur = gather(iq[0]);
-  for (long long step = 0; step < nstep; ++step) {
-    const int a = (int)(step % kPipe);
-    const long long r = r0 + step * kMidThreads + warp * 32 + lane;
-    long long s = 0, i1n = 0;
-    double v = 0.0;
+  for (long long step0 = 0; step0 < nstep; step0 += kPipe) {
 #pragma unroll
-    for (int q = 0; q < kPipe; ++q) {  // static register indexing of the ring slots
-      if (q == a) {
-        s = sq[q];
-        v = vq[q];
-        load_raw(r + kPipe * kMidThreads, sq[q], iq[q], vq[q]);  // the step kPipe ahead
+    for (int a = 0; a < kPipe; ++a) {
+      const long long step = step0 + a;
+      if (step >= nstep) break;  // block-uniform
+      const long long r = r0 + step * kMidThreads + warp * 32 + lane;
+      const long long s = sq[a];
+      const double w = __dmul_rn(vq[a], xcur);
+      load_raw(r + kPipe * kMidThreads, sq[a], iq[a], vq[a]);  // the step kPipe ahead
+      xcur = gather(iq[(a + 1) % kPipe]);  // next step's x, in flight during this step's turn
+      const bool valid = r < r1 && (unsigned long long)s < (unsigned long long)p.R;
+      const unsigned int m = __match_any_sync(0xffffffffu, valid ? s : -1 - lane);
+      const unsigned int rank = __popc(m & lt);
+      ring_take(warp, step);
+      unsigned int base = 0;
+      if (valid && rank == 0) {
+        base = cur[s];
+        cur[s] = base + __popc(m);
       }
-      if (q == (a + 1) % kPipe) i1n = iq[q];
+      ring_pass(warp, step, nstep);
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (valid) dst[base + rank] = w;
     }
-    const double w = __dmul_rn(v, xcur);
-    xcur = gather(i1n);  // next step's x, in flight during this step's turn
-    const bool valid = r < r1 && (unsigned long long)s < (unsigned long long)p.R;
-    const unsigned int m = __match_any_sync(0xffffffffu, valid ? s : -1 - lane);
-    const unsigned int rank = __popc(m & lt);
-    ring_take(warp, step);
-    unsigned int pos = 0;
-    if (valid) pos = cur[s] + rank;
-    __syncwarp();
-    if (valid && rank == 0) cur[s] = pos + __popc(m);
-    __syncwarp();
-    ring_pass(warp, step, nstep);
-    if (valid) dst[pos] = w;
   }
 }
 
@@ -412,22 +443,32 @@ __global__ void __launch_bounds__(kMidThreads) mid_scatter_kernel(MidParams p, l
   flush_counters(p, flags, 0);
 }
 
-// pass 3: fold every non-empty (i0, S) bucket.  Small buckets: one thread each; big ones are
-// queued for warp-cooperative folds.
+// pass 3: fold every non-empty (i0, S) bucket.  Buckets under kBigBucket rows: one thread each,
+// at once.  Longer ones are queued by size: bin j holds the buckets of [kBigBucket << j,
+// kBigBucket << (j + 1)) rows (one bucket per lane, 32 chains of similar length per warp -- a
+// single-lane chain costs a whole warp issue slot per add), buckets of >= kHugeBucket rows are
+// folded by a whole warp (coalesced loads far ahead of lane 0's chain).
 constexpr unsigned int kBigBucket = 64;
+constexpr unsigned int kHugeBucket = 4096;
+constexpr int kFoldBins = 6;  // log2(kHugeBucket / kBigBucket)
+
+struct FoldQueues {
+  unsigned long long* q;              // entries: class-B segment index << 32 | S
+  unsigned int* cnt;                  // [0..kFoldBins) bins, [kFoldBins] huge, [kFoldBins + 1] the fold kernel's ticket
+  unsigned int off[kFoldBins + 1];    // first entry of every queue
+};
 
 __global__ void mid_fold_kernel(MidParams p, const int* __restrict__ blist, const unsigned int* __restrict__ TOT,
                                 const unsigned int* __restrict__ BB, const unsigned int* __restrict__ GR,
-                                const double* __restrict__ w, unsigned long long* __restrict__ bigq,
-                                unsigned int* __restrict__ bign) {
+                                const double* __restrict__ w, FoldQueues fq) {
   const long long b = blockIdx.x;
   const long long s = (long long)blockIdx.y * blockDim.x + threadIdx.x;
   unsigned int zeros = 0;
   if (s < p.R) {
     const unsigned int n = TOT[b * p.R + s];
     if (n >= kBigBucket) {
-      const unsigned int q = atomicAdd(bign, 1u);
-      bigq[q] = ((unsigned long long)b << 32) | (unsigned long long)s;
+      const int bin = min(kFoldBins, 31 - __clz(n / kBigBucket));
+      fq.q[fq.off[bin] + atomicAdd(fq.cnt + bin, 1u)] = ((unsigned long long)b << 32) | (unsigned long long)s;
     } else if (n > 0) {
       const int i0 = blist[b];
       const long long start = p.off[i0] + BB[b * p.R + s];
@@ -440,28 +481,48 @@ __global__ void mid_fold_kernel(MidParams p, const int* __restrict__ blist, cons
   flush_counters(p, 0, zeros);
 }
 
-constexpr int kFoldAhead = 4;  // 32-row chunks of a big bucket in flight
-
+// Persistent warps take work by ticket, longest first: the huge buckets one per warp, then the
+// bins from the longest, 32 buckets per warp.  (A static round-robin over one queue resonated with
+// its (segment, S) order: with 148 * 64 warps every 37th segment's S = 0 bucket -- the longest
+// chains -- landed on the same warp.)
 __global__ void __launch_bounds__(256) mid_fold_big_kernel(MidParams p, const int* __restrict__ blist,
                                                            const unsigned int* __restrict__ TOT,
                                                            const unsigned int* __restrict__ BB,
                                                            const unsigned int* __restrict__ GR,
-                                                           const double* __restrict__ w,
-                                                           const unsigned long long* __restrict__ bigq,
-                                                           const unsigned int* __restrict__ bign) {
+                                                           const double* __restrict__ w, FoldQueues fq) {
   __shared__ __align__(16) double s_ring[8][kRingChunks * 32];
   const int lane = threadIdx.x & 31;
-  const unsigned int nq = *bign;
-  const unsigned int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const unsigned int nh = fq.cnt[kFoldBins];
   unsigned int zeros = 0;
-  for (unsigned int q = gw; q < nq; q += nw) {
-    const unsigned long long e = bigq[q];
-    const long long b = (long long)(e >> 32);
-    const long long s = (long long)(e & 0xffffffffu);
-    const long long n = TOT[b * p.R + s];
-    const int i0 = blist[b];
-    const double acc = warp_serial_fold(w + p.off[i0] + BB[b * p.R + s], n, s_ring[threadIdx.x >> 5]);
-    if (lane == 0) {
+  while (true) {
+    unsigned int t = 0;
+    if (lane == 0) t = atomicAdd(fq.cnt + kFoldBins + 1, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t < nh) {
+      const unsigned long long e = fq.q[fq.off[kFoldBins] + t];
+      const long long b = (long long)(e >> 32), s = (long long)(e & 0xffffffffu);
+      const int i0 = blist[b];
+      const double acc = warp_serial_fold(w + p.off[i0] + BB[b * p.R + s], TOT[b * p.R + s], s_ring[threadIdx.x >> 5]);
+      if (lane == 0) {
+        emit_group(p, p.out_base[i0] + GR[b * p.R + s], i0, s, acc);
+        zeros += acc == 0.0;
+      }
+      continue;
+    }
+    t -= nh;
+    int bin = kFoldBins - 1;
+    for (; bin >= 0; --bin) {
+      const unsigned int nw = (fq.cnt[bin] + 31) / 32;
+      if (t < nw) break;
+      t -= nw;
+    }
+    if (bin < 0) break;
+    const unsigned int idx = t * 32 + lane;
+    if (idx < fq.cnt[bin]) {
+      const unsigned long long e = fq.q[fq.off[bin] + idx];
+      const long long b = (long long)(e >> 32), s = (long long)(e & 0xffffffffu);
+      const int i0 = blist[b];
+      const double acc = lane_serial_fold(w + p.off[i0] + BB[b * p.R + s], TOT[b * p.R + s]);
       emit_group(p, p.out_base[i0] + GR[b * p.R + s], i0, s, acc);
       zeros += acc == 0.0;
     }
@@ -596,237 +657,123 @@ __global__ void __launch_bounds__(kMidThreads) mid_med_kernel(MidParams p, const
   flush_counters(p, flags, zeros);
 }
 
-// ---- class A: one CTA per window of kWin class-A rows ------------------------------------------
-struct WinSmem {
-  unsigned int key[2][kBufRows];      // seg_local << 14 | S
-  unsigned short li[2][kBufRows];     // local row (stable payload)
-  double w[kBufRows];                 // w by local row
-  union {
-    int seg_row0[kWin];                 // first row of every segment, while keys are built
-    unsigned short hw[kMidWarps][512];  // per-warp digit counts, then cursors, while sorting
-  };
-  int seg_i0[kWin];                   // class-A segments starting in the window
-  union {
-    int seg_base[kWin + 1];           // their first local row (exclusive scan), while keys are built
-    int seg_g0[kWin + 1];             // their first group (window-local), while groups are folded
-  };
-  unsigned long long ws[33];
-  int nseg, nrows, first;
-};
-
-template <int NS>
-__global__ void __launch_bounds__(kMidThreads) mid_window_kernel(MidParams p, const int* __restrict__ wfirst,
-                                                               long long nwin) {
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  WinSmem& S = *reinterpret_cast<WinSmem*>(s_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned int lt = (1u << lane) - 1u;
-  unsigned int flags = 0, zeros = 0;
-  // candidate segments: from this window's first class-A segment to the next window's
-  // (only the last window can hold no segment start: a class-A segment is shorter than a window,
-  // so it covers a whole window only when that window is cut short by the end of the rows)
-  const int first = wfirst[blockIdx.x];
-  if (first >= p.n0) return;
-  const int nxt = blockIdx.x + 1 < nwin ? wfirst[blockIdx.x + 1] : (int)p.n0;
-  const int cand = min(nxt, (int)p.n0) - first;
-  // class-A ones (1 <= L <= kWin), compacted in order; their rows concatenated.  Empty segments
-  // also "start" in the window, so the candidates come in rounds of kWin (at most kWin of them
-  // are non-empty: they start at distinct rows of the window).
-  int nseg_run = 0, nrows_run = 0;
-  for (int cb = 0; cb < cand; cb += kWin) {
-    constexpr int PER = kWin / kMidThreads;
-    int inc[PER], len[PER];
-    unsigned long long tot = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int c = cb + tid * PER + j;
-      len[j] = 0;
-      inc[j] = 0;
-      if (c < cand) {
-        const long long L = p.off[first + c + 1] - p.off[first + c];
-        if (L >= 1 && L <= kWin) {
-          inc[j] = 1;
-          len[j] = (int)L;
-        }
-      }
-      tot += ((unsigned long long)inc[j] << 32) | (unsigned long long)len[j];
-    }
-    unsigned long long total;
-    unsigned long long ex = block_excl_scan(tot, S.ws, &total);
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      if (inc[j]) {
-        const int k = nseg_run + (int)(ex >> 32);
-        S.seg_i0[k] = first + cb + tid * PER + j;
-        S.seg_base[k] = nrows_run + (int)(ex & 0xffffffffu);
-        S.seg_row0[k] = (int)p.off[first + cb + tid * PER + j];
-      }
-      ex += ((unsigned long long)inc[j] << 32) | (unsigned long long)len[j];
-    }
-    nseg_run += (int)(total >> 32);
-    nrows_run += (int)(total & 0xffffffffu);
-  }
-  if (tid == 0) {
-    S.nseg = nseg_run;
-    S.nrows = nrows_run;
-    S.seg_base[nseg_run] = nrows_run;
-  }
-  __syncthreads();
-  const int nseg = S.nseg, n = S.nrows;
-  if (nseg == 0) return;
-  // keys and w, local row by local row (coalesced within a segment); four rows per thread in
-  // flight: raw loads first, then the x gathers
-  for (int l0 = tid; l0 < n; l0 += 8 * kMidThreads) {
-    long long r[8], sk[8], i1[8];
-    double v[8];
-    int sl[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int li = l0 + u * kMidThreads;
-      sl[u] = 0;
-      r[u] = -1;
-      if (li < n) {
-        int lo = 0, hi = nseg - 1;  // segment of local row li: last base <= li
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (S.seg_base[mid] <= li) lo = mid;
-          else hi = mid - 1;
-        }
-        sl[u] = lo;
-        r[u] = S.seg_row0[lo] + (li - S.seg_base[lo]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (r[u] < 0) continue;
-      sk[u] = suffix_key<NS>(p, r[u], flags);
-      i1[u] = __ldg(p.c1 + r[u]);
-      v[u] = __ldg(p.vals + r[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (r[u] < 0) continue;
-      const int li = l0 + u * kMidThreads;
-      const bool bad = (unsigned long long)i1[u] >= (unsigned long long)p.n1;
-      if (bad) flags |= kFlagIndex;
-      S.w[li] = __dmul_rn(v[u], __ldg(p.x + (bad ? 0 : i1[u])));
-      S.key[0][li] = ((unsigned int)sl[u] << 14) | (unsigned int)max(0LL, min(sk[u], p.R - 1));
-      S.li[0][li] = (unsigned short)li;
-    }
-  }
-  __syncthreads();
-  // three stable LSD passes over the 25-bit (seg_local, S) key, 9-bit digits.  Each warp owns a
-  // contiguous block of the keys: per-warp digit counts, one scan over (digit, warp), then every
-  // warp scatters its block in order with its own cursors -- no cross-warp ordering needed.
-  int cur = 0;
-  const int blk = (n + kMidWarps - 1) / kMidWarps;
-  const int b0 = min(n, warp * blk), b1 = min(n, b0 + blk);
-  for (int shift = 0; shift < 27; shift += 9) {
-    for (int i = lane; i < 512; i += 32) S.hw[warp][i] = 0;
-    __syncwarp();
-    for (int i0c = b0; i0c < b1; i0c += 32) {
-      const int i = i0c + lane;
-      const unsigned int dg = i < b1 ? (S.key[cur][i] >> shift) & 511u : 512u + lane;
-      const unsigned int m = __match_any_sync(0xffffffffu, dg);
-      if (i < b1 && (m & lt) == 0) S.hw[warp][dg] += (unsigned short)__popc(m);
-      __syncwarp();
-    }
-    __syncthreads();
-    {  // cursor of (warp, digit) = all keys of smaller digits + this digit's keys in earlier warps
-      unsigned int c[2][kMidWarps], tot2 = 0;
-#pragma unroll
-      for (int d = 0; d < 2; ++d)
-#pragma unroll
-        for (int w8 = 0; w8 < kMidWarps; ++w8) {
-          c[d][w8] = S.hw[w8][2 * tid + d];
-          tot2 += c[d][w8];
-        }
-      unsigned long long total;
-      unsigned int run = (unsigned int)block_excl_scan((unsigned long long)tot2, S.ws, &total);
-#pragma unroll
-      for (int d = 0; d < 2; ++d)
-#pragma unroll
-        for (int w8 = 0; w8 < kMidWarps; ++w8) {
-          S.hw[w8][2 * tid + d] = (unsigned short)run;
-          run += c[d][w8];
-        }
-    }
-    __syncthreads();
-    for (int i0c = b0; i0c < b1; i0c += 32) {
-      const int i = i0c + lane;
-      const bool valid = i < b1;
-      const unsigned int key = valid ? S.key[cur][i] : 0u;
-      const unsigned short l = valid ? S.li[cur][i] : 0;
-      const unsigned int dg = valid ? (key >> shift) & 511u : 512u + lane;
-      const unsigned int m = __match_any_sync(0xffffffffu, dg);
-      const unsigned int rank = __popc(m & lt);
-      unsigned int pos = 0;
-      if (valid) pos = S.hw[warp][dg] + rank;
-      __syncwarp();
-      if (valid && rank == 0) S.hw[warp][dg] = (unsigned short)(pos + __popc(m));
-      __syncwarp();
-      if (valid) {
-        S.key[cur ^ 1][pos] = key;
-        S.li[cur ^ 1][pos] = l;
-      }
-    }
-    __syncthreads();
-    cur ^= 1;
-  }
-  // groups: runs of equal key; heads -> window-local group ids (block scan), segment first groups
-  const unsigned int* K = S.key[cur];
-  int* hp = reinterpret_cast<int*>(S.key[cur ^ 1]);  // head positions by group id (free buffer)
-  {
-    constexpr int PER = kBufRows / kMidThreads;
-    unsigned long long cnt = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = tid * PER + j;
-      cnt += (i < n && (i == 0 || K[i] != K[i - 1])) ? 1ull : 0ull;
-    }
-    unsigned long long total;
-    unsigned long long g = block_excl_scan(cnt, S.ws, &total);
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = tid * PER + j;
-      if (i < n && (i == 0 || K[i] != K[i - 1])) {
-        hp[g] = i;
-        if (i == 0 || (K[i] >> 14) != (K[i - 1] >> 14)) S.seg_g0[K[i] >> 14] = (int)g;
-        ++g;
-      }
-    }
-    if (tid == 0) hp[total] = n;
-    __syncthreads();
-    const int ng = (int)total;
-    for (int k = tid; k < nseg; k += kMidThreads) {
-      const int gend = k + 1 < nseg ? S.seg_g0[k + 1] : ng;
-      p.groups[S.seg_i0[k]] = gend - S.seg_g0[k];
-    }
-    // fold every group (one thread each), into the row-indexed scratch of its segment
-    for (int g2 = tid; g2 < ng; g2 += kMidThreads) {
-      const int a = hp[g2], e = hp[g2 + 1];
-      const unsigned int key = K[a];
-      const int sl = (int)(key >> 14);
-      double acc = S.w[S.li[cur][a]];
-      for (int i = a + 1; i < e; ++i) acc = __dadd_rn(acc, S.w[S.li[cur][i]]);
-      const int i0 = S.seg_i0[sl];
-      const long long row = p.abase[i0] + (g2 - S.seg_g0[sl]);
-      p.ti0[row] = i0;
-      p.tkey[row] = key & 0x3fffu;
-      p.tval[row] = acc;
-      zeros += acc == 0.0;
-    }
-  }
-  flush_counters(p, flags, zeros);
+// ---- class A: one warp per segment ------------------------------------------------------------
+// A segment of L <= kWarpMax rows holds at most L distinct S.  The warp marks the S present in a
+// bitmap over [0, R), turns it into ranks (prefix popcounts: the group of S is its rank among the
+// S present, which is also the output order), and then adds w = vals * x[i1] into acc[group] in
+// row order: per 32-row step the first lane of every distinct group loads the accumulator, adds
+// its own w and then the w of the later lanes of the same group in lane order (shuffles), and
+// stores it back -- the reference's left fold in original row order, started from -0.0 (the exact
+// additive identity).  No sort, no scratch, no CTA barrier.  COUNT: only the group count (the
+// output rows of every segment must be known before anything is written).
+constexpr int kWarpsPerCta = 8;
+__host__ __device__ constexpr size_t warp_smem_bytes(int W) {
+  return ((size_t)kWarpMax * 8 + (size_t)W * 4 + (size_t)W * 2 + (size_t)kWarpMax * 2 + 15) & ~(size_t)15;
 }
 
-// class-A groups: scratch (by class-A row; unwritten slots hold -1) -> final rows, thread per slot
-__global__ void mid_move_kernel(MidParams p, long long na) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < na; j += (long long)gridDim.x * blockDim.x) {
-    const int i0 = p.ti0[j];
-    if (i0 < 0) continue;
-    emit_group(p, p.out_base[i0] + (j - p.abase[i0]), i0, p.tkey[j], p.tval[j]);
+template <int NS, bool COUNT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p, const int* __restrict__ alist,
+                                                                     long long nseg) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  const int W = (int)((p.R + 31) >> 5);
+  unsigned char* mine = s_raw + (size_t)warp * warp_smem_bytes(W);
+  double* acc = reinterpret_cast<double*>(mine);
+  unsigned int* bm = reinterpret_cast<unsigned int*>(acc + kWarpMax);
+  unsigned short* pre = reinterpret_cast<unsigned short*>(bm + W);
+  unsigned short* skey = pre + W;
+  const int K = (W + 31) >> 5;  // bitmap words per lane in the rank scan
+  unsigned int flags = 0, zeros = 0;
+  for (long long q = (long long)blockIdx.x * kWarpsPerCta + warp; q < nseg; q += (long long)gridDim.x * kWarpsPerCta) {
+    const int i0 = alist[q];
+    const long long r0 = p.off[i0];
+    const int L = (int)(p.off[i0 + 1] - r0);
+    for (int i = lane; i < W; i += 32) bm[i] = 0;
+    __syncwarp();
+    for (int j = lane; j < L; j += 32) {
+      const long long s = max(0LL, min(suffix_key<NS>(p, r0 + j, flags), p.R - 1));
+      atomicOr(&bm[s >> 5], 1u << (s & 31));
+    }
+    __syncwarp();
+    int cnt = 0;
+    for (int k = 0; k < K; ++k) {
+      const int i = lane * K + k;
+      if (i < W) cnt += __popc(bm[i]);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int G = __shfl_sync(0xffffffffu, incl, 31);
+    if constexpr (COUNT) {
+      if (lane == 0) p.groups[i0] = G;
+      __syncwarp();
+      continue;
+    }
+    int run = incl - cnt;
+    for (int k = 0; k < K; ++k) {
+      const int i = lane * K + k;
+      if (i < W) {
+        pre[i] = (unsigned short)run;
+        run += __popc(bm[i]);
+      }
+    }
+    for (int g = lane; g < G; g += 32) acc[g] = -0.0;
+    __syncwarp();
+    // rows in order, 32 per step; the next step's raw loads are in flight during this one
+    long long sn = 0, i1n = 0;
+    double vn = 0.0;
+    if (lane < L) {
+      sn = suffix_key<NS>(p, r0 + lane, flags);
+      i1n = __ldcs(p.c1 + r0 + lane);
+      vn = __ldcs(p.vals + r0 + lane);
+    }
+    for (int j0 = 0; j0 < L; j0 += 32) {
+      const int j = j0 + lane;
+      const bool valid = j < L;
+      const long long s = max(0LL, min(sn, p.R - 1)), i1 = i1n;
+      const double v = vn;
+      if (j + 32 < L) {
+        sn = suffix_key<NS>(p, r0 + j + 32, flags);
+        i1n = __ldcs(p.c1 + r0 + j + 32);
+        vn = __ldcs(p.vals + r0 + j + 32);
+      }
+      const bool bad = (unsigned long long)i1 >= (unsigned long long)p.n1;
+      if (bad && valid) flags |= kFlagIndex;
+      const double w = __dmul_rn(v, __ldg(p.x + (bad || !valid ? 0 : i1)));
+      const unsigned int word = bm[s >> 5];
+      const int g = valid ? (int)pre[s >> 5] + __popc(word & ((1u << (s & 31)) - 1u)) : -1 - lane;
+      const unsigned int m = __match_any_sync(0xffffffffu, g);
+      const bool lead = valid && (m & lt) == 0;
+      double a = 0.0;
+      if (lead) {
+        a = __dadd_rn(acc[g], w);
+        skey[g] = (unsigned short)s;
+      }
+      unsigned int rem = lead ? m & ~(1u << lane) : 0u;  // the later rows of this group, in lane order
+      while (__any_sync(0xffffffffu, rem != 0u)) {
+        const int src = rem ? __ffs(rem) - 1 : lane;
+        const double wv = __shfl_sync(0xffffffffu, w, src);
+        if (rem) {
+          a = __dadd_rn(a, wv);
+          rem &= rem - 1;
+        }
+      }
+      if (lead) acc[g] = a;
+      __syncwarp();
+    }
+    const long long ob = p.out_base[i0];
+    for (int g = lane; g < G; g += 32) {
+      const double v = acc[g];
+      emit_group(p, ob + g, i0, skey[g], v);
+      zeros += v == 0.0;
+    }
+    __syncwarp();
   }
+  flush_counters(p, flags, zeros);
 }
 
 int mid_grid(long long n) { return (int)std::max(1LL, std::min((n + 255) / 256, (long long)num_sms() * 16)); }
@@ -841,7 +788,7 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
   const long long n0 = p.n0, R = p.R, nnz = p.nnz;
   // tests shrink these to put small data through every class and many tiles
   const long long tile_rows = env_ll("TK_MID_TILE", kTileRows);
-  p.med_max = std::min(kMedMax, std::max<long long>(kWin, env_ll("TK_MID_MEDMAX", kMedMax)));
+  p.med_max = std::min(kMedMax, std::max<long long>(kWarpMax, env_ll("TK_MID_MEDMAX", kMedMax)));
   long long* hv = static_cast<long long*>(pinned_scratch(sizeof(Counters) + 96));
   Counters* hc = reinterpret_cast<Counters*>(hv + 8);
   DevBuf b_ctr, b_off, b_plan, b_groups;
@@ -856,34 +803,30 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
   long long* tbase = isb + (n0 + 1);
   long long* cbase = tbase + (n0 + 1);
   long long* midx = cbase + (n0 + 1);
-  long long* abase = midx + (n0 + 1);
-  mid_classify_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, p.off, tile_rows, p.med_max, isb, tbase, cbase, midx, abase);
+  long long* aidx = midx + (n0 + 1);
+  mid_classify_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, p.off, tile_rows, p.med_max, isb, tbase, cbase, midx, aidx);
   count_launch(2);
   TK_CUDA(cudaGetLastError());
-  for (long long* a : {isb, tbase, cbase, midx, abase})
+  for (long long* a : {isb, tbase, cbase, midx, aidx})
     if (int rc = scan_excl_i64(a, a, n0, st)) return rc;  // [n0] = the totals
   TK_CUDA(cudaMemcpyAsync(hc, p.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   int j = 0;
-  for (long long* a : {isb, tbase, cbase, midx, abase}) TK_CUDA(cudaMemcpyAsync(hv + j++, a + n0, 8, cudaMemcpyDeviceToHost, st));
+  for (long long* a : {isb, tbase, cbase, midx, aidx}) TK_CUDA(cudaMemcpyAsync(hv + j++, a + n0, 8, cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
   if (hc->flags) return kMidDeclined;  // unsorted or out-of-range leading column
   const long long nb = hv[0], ntiles = hv[1], nchunks = hv[2], nm = hv[3], na = hv[4];
-  const long long nwin = (na + kWin - 1) / kWin;
-  p.abase = abase;
 
   if (int rc = b_groups.alloc((size_t)(n0 + 1) * 8, st)) return rc;
   TK_CUDA(cudaMemsetAsync(b_groups.get(), 0, (size_t)(n0 + 1) * 8, st));
   p.groups = b_groups.as<long long>();
-  DevBuf b_lists, b_H, b_P, b_TOT, b_BB, b_GR, b_w, b_bigq, b_bign, b_ti0, b_tkey, b_tval;
-  if (int rc = b_lists.alloc((size_t)(nb + ntiles + nchunks + nm + nwin + 4) * 4, st)) return rc;
+  DevBuf b_lists, b_H, b_P, b_TOT, b_BB, b_GR, b_w, b_bigq, b_bign;
+  if (int rc = b_lists.alloc((size_t)(nb + ntiles + nchunks + nm + na + 4) * 4, st)) return rc;
   int* blist = b_lists.as<int>();
   int* tseg = blist + nb;
   int* cseg = tseg + ntiles;
   int* mlist = cseg + nchunks;
-  int* wfirst = mlist + nm;
-  TK_CUDA(cudaMemsetAsync(wfirst, 0x7f, (size_t)(nwin + 1) * 4, st));
-  mid_lists_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, p.off, isb, tbase, cbase, midx, abase, blist, tseg, cseg, mlist,
-                                                 wfirst);
+  int* alist = mlist + nm;
+  mid_lists_kernel<<<mid_grid(n0), 256, 0, st>>>(n0, isb, tbase, cbase, midx, aidx, blist, tseg, cseg, mlist, alist);
   count_launch();
   const dim3 blk(256);
   const unsigned int ry = (unsigned int)((R + 255) / 256);
@@ -914,38 +857,39 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
     mid_med_count_kernel<NS><<<(unsigned int)nm, kMidThreads, hsm, st>>>(p, mlist);
     count_launch();
   }
-  // ---- class A: windows -> scratch by class-A row + group counts
-  if (nwin > 0) {
-    if (int rc = b_ti0.alloc((size_t)na * 4, st)) return rc;
-    if (int rc = b_tkey.alloc((size_t)na * 4, st)) return rc;
-    if (int rc = b_tval.alloc((size_t)na * 8, st)) return rc;
-    p.ti0 = b_ti0.as<int>();
-    p.tkey = b_tkey.as<unsigned int>();
-    p.tval = b_tval.as<double>();
-    TK_CUDA(cudaMemsetAsync(p.ti0, 0xff, (size_t)na * 4, st));
-    TK_CUDA(cudaFuncSetAttribute(mid_window_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(WinSmem)));
-    mid_window_kernel<NS><<<(unsigned int)nwin, kMidThreads, sizeof(WinSmem), st>>>(p, wfirst, nwin);
+  // ---- class A: group counts
+  const size_t wsm = kWarpsPerCta * warp_smem_bytes((int)((R + 31) / 32));
+  const unsigned int wgrid = (unsigned int)std::max(1LL, std::min((na + kWarpsPerCta - 1) / kWarpsPerCta, (long long)num_sms() * 4));
+  if (na > 0) {
+    TK_CUDA(cudaFuncSetAttribute(mid_warp_kernel<NS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    TK_CUDA(cudaFuncSetAttribute(mid_warp_kernel<NS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    mid_warp_kernel<NS, true><<<wgrid, kWarpsPerCta * 32, wsm, st>>>(p, alist, na);
     count_launch();
   }
   TK_CUDA(cudaGetLastError());
   if (int rc = scan_excl_i64(p.groups, p.groups, n0, st)) return rc;  // -> out_base, [n0] = groups
   p.out_base = p.groups;
-  // ---- class B and M: scatter + folds straight to the output rows; class A: the move
+  // ---- every class: straight to the output rows
   if (nb > 0 || nm > 0)
     if (int rc = b_w.alloc((size_t)nnz * 8, st)) return rc;
   if (nb > 0) {
-    if (int rc = b_bigq.alloc(((size_t)nnz / kBigBucket + 64) * 8, st)) return rc;
-    if (int rc = b_bign.alloc(16, st)) return rc;
-    TK_CUDA(cudaMemsetAsync(b_bign.get(), 0, 16, st));
+    FoldQueues fq{};
+    size_t qtot = 0;
+    for (int j = 0; j <= kFoldBins; ++j) {  // a queue of buckets of >= kBigBucket << j rows
+      fq.off[j] = (unsigned int)qtot;
+      qtot += (size_t)nnz / ((size_t)kBigBucket << j) + 64;
+    }
+    if (int rc = b_bigq.alloc(qtot * 8, st)) return rc;
+    if (int rc = b_bign.alloc(64, st)) return rc;
+    TK_CUDA(cudaMemsetAsync(b_bign.get(), 0, 64, st));
+    fq.q = b_bigq.as<unsigned long long>();
+    fq.cnt = b_bign.as<unsigned int>();
     mid_scatter_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm, st>>>(
         p, tile_rows, tseg, tbase, isb, b_H.as<unsigned int>(), b_BB.as<unsigned int>(), b_w.as<double>());
     mid_fold_kernel<<<dim3((unsigned int)nb, ry), blk, 0, st>>>(p, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
-                                                                b_GR.as<unsigned int>(), b_w.as<double>(),
-                                                                b_bigq.as<unsigned long long>(), b_bign.as<unsigned int>());
+                                                                b_GR.as<unsigned int>(), b_w.as<double>(), fq);
     mid_fold_big_kernel<<<num_sms() * 8, 256, 0, st>>>(p, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
-                                                       b_GR.as<unsigned int>(), b_w.as<double>(),
-                                                       b_bigq.as<unsigned long long>(), b_bign.as<unsigned int>());
+                                                       b_GR.as<unsigned int>(), b_w.as<double>(), fq);
     count_launch(3);
   }
   if (nm > 0) {
@@ -954,7 +898,7 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
     count_launch();
   }
   if (na > 0) {
-    mid_move_kernel<<<mid_grid(na), 256, 0, st>>>(p, na);
+    mid_warp_kernel<NS, false><<<wgrid, kWarpsPerCta * 32, wsm, st>>>(p, alist, na);
     count_launch();
   }
   TK_CUDA(cudaGetLastError());

@@ -18,7 +18,9 @@ x = uniform_vector(shape[1], 778)
 os_ = torch.empty((nnz, 2), dtype=torch.int64, device="cuda")
 ov = torch.empty(nnz, dtype=torch.float64, device="cuda")
 res = {}
-for mode in ("1", "0"):
+only = os.environ.get("TK_MID_ONLY") == "1"  # skip the CUB comparison (profiling runs)
+same = None
+for mode in (("1",) if only else ("1", "0")):
     os.environ["TK_MID_MODE"] = mode
     ts = []
     l0 = _lib.load().tk_launch_count()
@@ -38,4 +40,4 @@ for mode in ("1", "0"):
         same = torch.equal(ref[0], os_[:u]) and torch.equal(ref[1].view(torch.int64), ov[:u].view(torch.int64))
 b = nnz * 32 + 8 * shape[1] + res["1"][1] * 24
 print(f"counting path: {res['1'][0]:.3f} ms ({b / res['1'][0] / 1e6:.0f} GB/s alg, {res['1'][2]:.0f} launches), "
-      f"CUB split path: {res['0'][0]:.3f} ms, u={res['1'][1]}, identical={same}")
+      + (f"u={res['1'][1]}" if only else f"CUB split path: {res['0'][0]:.3f} ms, u={res['1'][1]}, identical={same}"))
