@@ -55,7 +55,6 @@ constexpr long long kMidMaxR = 16384;  // suffix key S < 2^14
 constexpr int kChunkTiles = 32;        // column scan: tiles per chunk
 constexpr long long kMedMax = 65536;   // class M: segments of kWarpMax+1 .. kMedMax rows
 constexpr long long kTileRows = 262144;  // class B counting tile (long runs per bucket: full-sector writes)
-constexpr int kMedBigList = kMedMax / 24;  // class M: warp-folded buckets of one segment
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -252,65 +251,140 @@ __global__ void mid_lists_kernel(long long n0, const long long* __restrict__ bid
   }
 }
 
-// Streams rows [r0, r1) in 256-row steps (warp w takes rows step*256 + 32w + lane) and scatters
-// w = vals * x[i1] stably to dst[cur[S]++] (token ring: the eight warps update the cursors in
-// turn, ranks inside a warp step from __match_any_sync).  The raw loads (S columns, i1, vals) are
-// issued kPipe steps ahead and the x gather one step ahead, so no instruction waits on a load
-// issued in the same step; the step loop is unrolled by kPipe so the look-ahead slots are
-// registers (a runtime slot index put them in local memory: 35% of the stall samples).  A warp's
-// turn is one shared load and one store by the first lane of every distinct S; the other lanes
-// take their bucket's base from that lane afterwards.
-constexpr int kPipe = 4;
+// ---- streaming skeleton shared by class B (stable scatter) and class M (ordered accumulate) ----
+// Rows [r0, r1) go through the CTA in chunks of kChunk rows.  All threads load a chunk coalesced
+// (raw columns one chunk ahead in registers, the x gathers of the next chunk in flight during the
+// current one) and form (S, w = vals * x[i1]).  The chunk is then split stably by OWNER -- warp
+// S % 8 owns S -- into eight contiguous lists in shared memory: every thread ranks its rows inside
+// its 32-row step (one match per step), the step leaders leave the step's per-owner counts, one
+// warp scans the 256 counts (owner-major, steps in row order), and every row goes to its slot.
+// Each warp then walks its own list in dense 32-row steps.  All rows of one S pass through one
+// warp in row order, so the warps never order themselves against each other (no token ring), and a
+// step holds only S of its warp.
+constexpr int kRowsPerThread = 4;
+constexpr int kChunk = kRowsPerThread * kMidThreads;
+constexpr int kSteps = kChunk / 32;  // 32-row steps of a chunk, in row order: step = k * kMidWarps + warp
+static_assert(kSteps == 32 && kMidWarps == 8, "the count scan gives one lane eight counters of one owner");
 
-template <int NS>
-__device__ __forceinline__ void stream_scatter(const MidParams& p, long long r0, long long r1, unsigned int* cur,
-                                               double* __restrict__ dst, unsigned int& flags) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+struct StreamSmem {  // carved from dynamic shared memory by the kernels
+  double* lw;           // kChunk
+  unsigned short* ls;   // kChunk
+  unsigned short* cnt;  // kMidWarps * kSteps, zero between chunks
+  unsigned short* offs; // kMidWarps * kSteps + kMidWarps + 1: slot of (owner, step); list starts; total
+};
+__host__ __device__ constexpr size_t stream_smem_bytes() {
+  return (size_t)kChunk * 10 + (size_t)kMidWarps * kSteps * 4 + 32;
+}
+__device__ __forceinline__ StreamSmem stream_carve(double* lw_aligned8, unsigned short* u16_area) {
+  StreamSmem sm;
+  sm.lw = lw_aligned8;
+  sm.ls = u16_area;
+  sm.cnt = sm.ls + kChunk;
+  sm.offs = sm.cnt + kMidWarps * kSteps;
+  return sm;
+}
+
+template <int NS, class Proc>
+__device__ __forceinline__ void stream_owned(const MidParams& p, long long r0, long long r1, const StreamSmem& sm,
+                                             unsigned int& flags, Proc&& proc) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned int lt = (1u << lane) - 1u;
-  const long long nstep = (r1 - r0 + kMidThreads - 1) / kMidThreads;
-  long long sq[kPipe], iq[kPipe];
-  double vq[kPipe];
-  auto load_raw = [&](long long r, long long& s, long long& i1, double& v) {
-    if (r < r1) {
-      s = suffix_key<NS>(p, r, flags);
-      i1 = __ldcs(p.c1 + r);
-      v = __ldcs(p.vals + r);
-    } else {
-      s = -1 - lane;
-      i1 = 0;
-      v = 0.0;
+  long long sA[kRowsPerThread], iA[kRowsPerThread];
+  double vA[kRowsPerThread], vB[kRowsPerThread], xB[kRowsPerThread];
+  unsigned short sB[kRowsPerThread];
+  auto load_raw = [&](long long cbase) {
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const long long r = cbase + k * kMidThreads + tid;
+      if (r < r1) {
+        sA[k] = suffix_key<NS>(p, r, flags);
+        iA[k] = __ldcs(p.c1 + r);
+        vA[k] = __ldcs(p.vals + r);
+      } else {
+        sA[k] = 0;
+        iA[k] = 0;
+        vA[k] = 0.0;
+      }
     }
   };
-  auto gather = [&](long long i1) {
-    const bool bad = (unsigned long long)i1 >= (unsigned long long)p.n1;
-    if (bad) flags |= kFlagIndex;
-    return __ldg(p.x + (bad ? 0 : i1));
+  auto advance = [&](long long cbase) {  // raw registers (chunk at cbase) -> S, value, x gather in flight
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const long long r = cbase + k * kMidThreads + tid;
+      const bool bad = (unsigned long long)iA[k] >= (unsigned long long)p.n1;
+      if (bad && r < r1) flags |= kFlagIndex;
+      sB[k] = (unsigned short)max(0LL, min(sA[k], p.R - 1));  // out of range: flagged by suffix_key, the call declines
+      vB[k] = vA[k];
+      xB[k] = __ldg(p.x + (bad || r >= r1 ? 0 : iA[k]));
+    }
   };
+  for (int i = tid; i < kMidWarps * kSteps; i += kMidThreads) sm.cnt[i] = 0;
+  load_raw(r0);
+  advance(r0);
+  load_raw(r0 + kChunk);
+  __syncthreads();
+  for (long long cbase = r0; cbase < r1; cbase += kChunk) {
+    // 1. rank of every row among the rows of its owner inside its 32-row step; per-step counts
+    unsigned short sv[kRowsPerThread];
+    double w[kRowsPerThread];
+    int slot[kRowsPerThread];  // owner * kSteps + step, then the list slot; -1: no row
 #pragma unroll
-  for (int a = 0; a < kPipe; ++a) load_raw(r0 + a * kMidThreads + warp * 32 + lane, sq[a], iq[a], vq[a]);
-  double xcur = gather(iq[0]);
-  for (long long step0 = 0; step0 < nstep; step0 += kPipe) {
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const bool valid = cbase + k * kMidThreads + tid < r1;
+      sv[k] = sB[k];
+      w[k] = __dmul_rn(vB[k], xB[k]);
+      const int owner = sv[k] % kMidWarps;
+      const unsigned int m = __match_any_sync(0xffffffffu, valid ? owner : kMidWarps + lane);
+      const int rank = __popc(m & lt);
+      const int cell = owner * kSteps + k * kMidWarps + warp;
+      if (valid && rank == 0) sm.cnt[cell] = (unsigned short)__popc(m);
+      slot[k] = valid ? (cell << 8) | rank : -1;
+    }
+    __syncthreads();
+    if (cbase + kChunk < r1) {  // the next chunk's gathers and the raw loads after it
+      advance(cbase + kChunk);
+      load_raw(cbase + 2 * kChunk);
+    }
+    // 2. warp 0: exclusive scan of the counts, owner-major (lane l: owner l / 4, eight steps)
+    if (warp == 0) {
+      int v[8], run = 0;
 #pragma unroll
-    for (int a = 0; a < kPipe; ++a) {
-      const long long step = step0 + a;
-      if (step >= nstep) break;  // block-uniform
-      const long long r = r0 + step * kMidThreads + warp * 32 + lane;
-      const long long s = sq[a];
-      const double w = __dmul_rn(vq[a], xcur);
-      load_raw(r + kPipe * kMidThreads, sq[a], iq[a], vq[a]);  // the step kPipe ahead
-      xcur = gather(iq[(a + 1) % kPipe]);  // next step's x, in flight during this step's turn
-      const bool valid = r < r1 && (unsigned long long)s < (unsigned long long)p.R;
-      const unsigned int m = __match_any_sync(0xffffffffu, valid ? s : -1 - lane);
-      const unsigned int rank = __popc(m & lt);
-      ring_take(warp, step);
-      unsigned int base = 0;
-      if (valid && rank == 0) {
-        base = cur[s];
-        cur[s] = base + __popc(m);
+      for (int q = 0; q < 8; ++q) {
+        v[q] = sm.cnt[lane * 8 + q];
+        sm.cnt[lane * 8 + q] = 0;
+        run += v[q];
       }
-      ring_pass(warp, step, nstep);
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      if (valid) dst[base + rank] = w;
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      int ex = incl - run;
+      if ((lane & 3) == 0) sm.offs[kMidWarps * kSteps + (lane >> 2)] = (unsigned short)ex;  // list start of the owner
+      if (lane == 31) sm.offs[kMidWarps * kSteps + kMidWarps] = (unsigned short)incl;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        sm.offs[lane * 8 + q] = (unsigned short)ex;
+        ex += v[q];
+      }
+    }
+    __syncthreads();
+    // 3. every row to its slot
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      if (slot[k] >= 0) {
+        const int pos = sm.offs[slot[k] >> 8] + (slot[k] & 255);
+        sm.ls[pos] = sv[k];
+        sm.lw[pos] = w[k];
+      }
+    }
+    __syncthreads();
+    // 4. the warp's own list, in order
+    const int e0 = sm.offs[kMidWarps * kSteps + warp], e1 = sm.offs[kMidWarps * kSteps + warp + 1];
+    for (int e = e0; e < e1; e += 32) {
+      const int i = min(e + lane, e1 - 1);
+      proc(sm.ls[i], sm.lw[i], e + lane < e1);
     }
   }
 }
@@ -418,8 +492,8 @@ __global__ void __launch_bounds__(1024) mid_segscan_kernel(long long R, const in
   if (threadIdx.x == 0) groups[blist[b]] = (long long)(total >> 32);
 }
 
-// pass 2: stable scatter of w into every bucket's row range, in original row order
-
+// pass 2: stable scatter of w into every bucket's row range, in original row order.  The cursor
+// of S is touched only by the warp that owns S, in row order.
 template <int NS>
 __global__ void __launch_bounds__(kMidThreads) mid_scatter_kernel(MidParams p, long long tile_rows,
                                                                 const int* __restrict__ tile_seg,
@@ -428,8 +502,12 @@ __global__ void __launch_bounds__(kMidThreads) mid_scatter_kernel(MidParams p, l
                                                                 const unsigned int* __restrict__ H,
                                                                 const unsigned int* __restrict__ BB,
                                                                 double* __restrict__ wout) {
-  extern __shared__ unsigned int s_dyn[];
-  unsigned int* s_cur = s_dyn;  // per S: next output row (absolute)
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  double* lw = reinterpret_cast<double*>(s_raw);
+  unsigned int* s_cur = reinterpret_cast<unsigned int*>(lw + kChunk);  // per S: next output row
+  const StreamSmem sm = stream_carve(lw, reinterpret_cast<unsigned short*>(s_cur + p.R));
+  const int lane = threadIdx.x & 31;
+  const unsigned int lt = (1u << lane) - 1u;
   const long long t = blockIdx.x;
   const int i0 = tile_seg[t];
   const long long r0 = p.off[i0] + (t - tbase[i0]) * tile_rows;
@@ -437,9 +515,19 @@ __global__ void __launch_bounds__(kMidThreads) mid_scatter_kernel(MidParams p, l
   const long long b = bidx[i0];
   const unsigned int seg0 = (unsigned int)p.off[i0];
   for (long long s = threadIdx.x; s < p.R; s += blockDim.x) s_cur[s] = seg0 + BB[b * p.R + s] + H[t * p.R + s];
-  __syncthreads();
   unsigned int flags = 0;
-  stream_scatter<NS>(p, r0, r1, s_cur, wout, flags);
+  auto step = [&](unsigned short sv, double w, bool valid) {
+    const unsigned int m = __match_any_sync(0xffffffffu, valid ? (int)sv : -1 - lane);
+    const unsigned int rank = __popc(m & lt);
+    unsigned int base = 0;
+    if (valid && rank == 0) {
+      base = s_cur[sv];
+      s_cur[sv] = base + __popc(m);
+    }
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (valid) wout[base + rank] = w;
+  };
+  stream_owned<NS>(p, r0, r1, sm, flags, step);
   flush_counters(p, flags, 0);
 }
 
@@ -531,127 +619,147 @@ __global__ void __launch_bounds__(256) mid_fold_big_kernel(MidParams p, const in
 }
 
 // ---- class M: one CTA per segment -----------------------------------------------------------------
+// w = vals * x[i1] is added into acc[S] (one accumulator per possible S, in shared memory) in row
+// order through the streaming skeleton: the warp that owns S packs each dense step's rows by S
+// (groups matched inside the step, a warp scan of the group sizes gives every S a contiguous run in
+// row order), and the first lane of an S loads the accumulator, adds its run left to right and
+// stores it -- the reference's fold, started from -0.0 (the exact additive identity).  A bitmap of
+// the S seen gives the output order (rank of S) at the end.  COUNT pass first: the bitmap alone.
+
+// marks the S of rows [r0, r1) in the zeroed bitmap (test first: most rows repeat an S already set)
 template <int NS>
-__global__ void __launch_bounds__(kMidThreads) mid_med_count_kernel(MidParams p, const int* __restrict__ mlist) {
-  extern __shared__ unsigned int s_dyn[];
-  unsigned int* hist = s_dyn;
-  __shared__ unsigned long long ws[33];
-  const int i0 = mlist[blockIdx.x];
-  const long long r0 = p.off[i0], r1 = p.off[i0 + 1];
-  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) hist[s] = 0;
-  __syncthreads();
-  unsigned int flags = 0;
-  for (long long r = r0 + threadIdx.x; r < r1; r += 4 * blockDim.x) {
+__device__ __forceinline__ void mark_bitmap(const MidParams& p, long long r0, long long r1, unsigned int* bm,
+                                            unsigned int& flags) {
+  for (long long r = r0 + threadIdx.x; r < r1; r += 4 * kMidThreads) {
     long long s[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s[u] = r + u * blockDim.x < r1 ? suffix_key<NS>(p, r + u * blockDim.x, flags) : -1;
+    for (int u = 0; u < 4; ++u)
+      s[u] = r + u * kMidThreads < r1 ? max(0LL, min(suffix_key<NS>(p, r + u * kMidThreads, flags), p.R - 1)) : -1;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if ((unsigned long long)s[u] < (unsigned long long)p.R) atomicAdd(&hist[s[u]], 1u);
+      if (s[u] >= 0) {
+        const unsigned int bit = 1u << (s[u] & 31);
+        if (!(bm[s[u] >> 5] & bit)) atomicOr(&bm[s[u] >> 5], bit);
+      }
   }
-  __syncthreads();
-  unsigned long long nz = 0;
-  for (long long s = threadIdx.x; s < p.R; s += blockDim.x) nz += hist[s] != 0;
-  unsigned long long total;
-  block_excl_scan(nz, ws, &total);
-  if (threadIdx.x == 0) p.groups[i0] = (long long)total;
-  flush_counters(p, flags, 0);
+}
+
+// warp 0: pre[i] = set bits in words [0, i) (skipped when pre is null); the total in every lane
+__device__ __forceinline__ int bitmap_ranks(const unsigned int* bm, unsigned short* pre, int W) {
+  const int lane = threadIdx.x & 31;
+  const int K = (W + 31) >> 5;
+  int cnt = 0;
+  for (int k = 0; k < K; ++k) {
+    const int i = lane * K + k;
+    if (i < W) cnt += __popc(bm[i]);
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (pre) {
+    int run = incl - cnt;
+    for (int k = 0; k < K; ++k) {
+      const int i = lane * K + k;
+      if (i < W) {
+        pre[i] = (unsigned short)run;
+        run += __popc(bm[i]);
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
 }
 
 template <int NS>
-__global__ void __launch_bounds__(kMidThreads) mid_med_kernel(MidParams p, const int* __restrict__ mlist,
-                                                            double* __restrict__ wout) {
-  extern __shared__ unsigned int s_dyn[];
-  unsigned int* start = s_dyn;      // per S: first row of the bucket (segment-relative)
-  unsigned int* cur = s_dyn + p.R;  // per S: next row to fill
-  __shared__ unsigned long long ws[33];
+__global__ void __launch_bounds__(kMidThreads) mid_cta_count_kernel(MidParams p, const int* __restrict__ mlist) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  unsigned int* bm = reinterpret_cast<unsigned int*>(s_raw);
   const int i0 = mlist[blockIdx.x];
-  const long long r0 = p.off[i0], r1 = p.off[i0 + 1];
+  const int W = (int)((p.R + 31) >> 5);
+  for (int i = threadIdx.x; i < W; i += kMidThreads) bm[i] = 0;
+  __syncthreads();
+  unsigned int flags = 0;
+  mark_bitmap<NS>(p, p.off[i0], p.off[i0 + 1], bm, flags);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int G = bitmap_ranks(bm, nullptr, W);
+    if (threadIdx.x == 0) p.groups[i0] = G;
+  }
+  flush_counters(p, flags, 0);
+}
+
+__host__ __device__ constexpr size_t cta_smem_bytes(long long R) {
+  return (size_t)R * 8 + (size_t)kMidWarps * 32 * 8 + stream_smem_bytes() + (size_t)((R + 31) / 32) * 6 + 16;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kMidThreads) mid_cta_kernel(MidParams p, const int* __restrict__ mlist) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int W = (int)((p.R + 31) >> 5);
+  double* acc = reinterpret_cast<double*>(s_raw);
+  double* runs = acc + p.R;
+  double* lw = runs + kMidWarps * 32;
+  unsigned int* bm = reinterpret_cast<unsigned int*>(lw + kChunk);
+  unsigned short* pre = reinterpret_cast<unsigned short*>(bm + W);
+  const StreamSmem sm = stream_carve(lw, pre + W + (W & 1));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned int lt = (1u << lane) - 1u;
+  const int i0 = mlist[blockIdx.x];
+  const long long r0 = p.off[i0], r1 = p.off[i0 + 1];
+  for (long long s = tid; s < p.R; s += kMidThreads) acc[s] = -0.0;
+  for (int i = tid; i < W; i += kMidThreads) bm[i] = 0;
+  double* run = runs + warp * 32;
   unsigned int flags = 0, zeros = 0;
-  for (long long s = tid; s < p.R; s += blockDim.x) cur[s] = 0;
-  __syncthreads();
-  for (long long r = r0 + tid; r < r1; r += 4 * blockDim.x) {
-    long long s[4];
+  auto step = [&](unsigned short sv, double w, bool valid) {
+    const unsigned int m = __match_any_sync(0xffffffffu, valid ? (int)sv : -1 - lane);
+    const int rank = __popc(m & lt);
+    const int n = valid && rank == 0 ? __popc(m) : 0;
+    int incl = n;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s[u] = r + u * blockDim.x < r1 ? suffix_key<NS>(p, r + u * blockDim.x, flags) : -1;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if ((unsigned long long)s[u] < (unsigned long long)p.R) atomicAdd(&cur[s[u]], 1u);
-  }
-  __syncthreads();
-  // bucket starts: exclusive scan of the counts over S, each thread a contiguous range of S
-  const long long per = (p.R + kMidThreads - 1) / kMidThreads;
-  const long long sa = min(p.R, (long long)tid * per), se = min(p.R, sa + per);
-  {
-    unsigned long long c = 0;
-    for (long long s = sa; s < se; ++s) c += cur[s];
-    unsigned long long total;
-    unsigned long long ex = block_excl_scan(c, ws, &total);
-    for (long long s = sa; s < se; ++s) {
-      const unsigned int n = cur[s];
-      start[s] = (unsigned int)ex;
-      cur[s] = (unsigned int)ex;
-      ex += n;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-  }
-  __syncthreads();
-  // stable scatter of w into the segment's rows of the scratch (token ring)
-  stream_scatter<NS>(p, r0, r1, cur, wout + r0, flags);
-  __syncthreads();  // the block's scattered w are visible to the block
-  // fold every non-empty bucket at its output row.  Ranks come from a scan over contiguous S
-  // ranges and are packed into start[] (rows and ranks < 2^16); the folds then take S striped
-  // over the threads (the Zipf-heavy small S spread out), buckets of >= kMedWarpFold rows queued
-  // for the warps (warp_serial_fold).
-  constexpr unsigned int kMedWarpFold = 24;
-  __shared__ unsigned int s_big[kMedBigList];
-  __shared__ unsigned int s_nbig;
-  __shared__ __align__(16) double s_ring[kMidWarps][kRingChunks * 32];
-  if (tid == 0) s_nbig = 0;
-  {
-    unsigned long long c = 0;
-    for (long long s = sa; s < se; ++s) c += cur[s] != start[s];
-    unsigned long long total;
-    unsigned int g = (unsigned int)block_excl_scan(c, ws, &total);
-    for (long long s = sa; s < se; ++s)
-      if (cur[s] != start[s]) start[s] |= (g++) << 16;
-  }
-  __syncthreads();
-  const long long gbase = p.out_base[i0];
-  const double* src = wout + r0;
-  for (long long s = tid; s < p.R; s += kMidThreads) {
-    const unsigned int st0 = start[s], a0 = st0 & 0xffffu, e = cur[s];
-    if (a0 == e) continue;
-    if (e - a0 >= kMedWarpFold) {
-      s_big[atomicAdd(&s_nbig, 1u)] = (unsigned int)s;
-      continue;
-    }
-    double acc = src[a0];
-    unsigned int j = a0 + 1;
-    for (; j + 4 <= e; j += 4) {  // independent loads ahead of the dependent adds
-      const double v0 = src[j], v1 = src[j + 1], v2 = src[j + 2], v3 = src[j + 3];
-      acc = __dadd_rn(acc, v0);
-      acc = __dadd_rn(acc, v1);
-      acc = __dadd_rn(acc, v2);
-      acc = __dadd_rn(acc, v3);
-    }
-    for (; j < e; ++j) acc = __dadd_rn(acc, src[j]);
-    emit_group(p, gbase + (st0 >> 16), i0, s, acc);
-    zeros += acc == 0.0;
-  }
-  __syncthreads();
-  {
-    const int warp = tid >> 5, lane = tid & 31;
-    const unsigned int nbig = s_nbig;
-    for (unsigned int k = warp; k < nbig; k += kMidWarps) {
-      const long long s = s_big[k];
-      const unsigned int st0 = start[s], a0 = st0 & 0xffffu;
-      const double acc = warp_serial_fold(src + a0, cur[s] - a0, s_ring[warp]);
-      if (lane == 0) {
-        emit_group(p, gbase + (st0 >> 16), i0, s, acc);
-        zeros += acc == 0.0;
+    const int off = incl - n;
+    const int goff = __shfl_sync(0xffffffffu, off, __ffs(m) - 1);
+    if (valid) run[goff + rank] = w;
+    __syncwarp();
+    if (n > 0) {
+      const double* q = run + off;
+      double a = __dadd_rn(acc[sv], q[0]);
+      int j = 1;
+      for (; j + 4 <= n; j += 4) {  // four loads ahead of four dependent adds
+        const double v0 = q[j], v1 = q[j + 1], v2 = q[j + 2], v3 = q[j + 3];
+        a = __dadd_rn(a, v0);
+        a = __dadd_rn(a, v1);
+        a = __dadd_rn(a, v2);
+        a = __dadd_rn(a, v3);
       }
+      for (; j < n; ++j) a = __dadd_rn(a, q[j]);
+      acc[sv] = a;
+      const unsigned int bit = 1u << (sv & 31);
+      if (!(bm[sv >> 5] & bit)) atomicOr(&bm[sv >> 5], bit);
+    }
+    __syncwarp();
+  };
+  __syncthreads();
+  stream_owned<NS>(p, r0, r1, sm, flags, step);
+  __syncthreads();
+  if (warp == 0) bitmap_ranks(bm, pre, W);
+  __syncthreads();
+  const long long obase = p.out_base[i0];
+  for (int i = tid; i < W; i += kMidThreads) {
+    unsigned int word = bm[i];
+    int g = pre[i];
+    while (word) {
+      const int bit = __ffs(word) - 1;
+      word &= word - 1;
+      const double v = acc[i * 32 + bit];
+      emit_group(p, obase + g, i0, (long long)i * 32 + bit, v);
+      zeros += v == 0.0;
+      ++g;
     }
   }
   flush_counters(p, flags, zeros);
@@ -839,7 +947,8 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
     if (int rc = b_BB.alloc((size_t)nb * R * 4, st)) return rc;
     if (int rc = b_GR.alloc((size_t)nb * R * 4, st)) return rc;
     TK_CUDA(cudaFuncSetAttribute(mid_hist_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-    TK_CUDA(cudaFuncSetAttribute(mid_scatter_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    TK_CUDA(cudaFuncSetAttribute(mid_scatter_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(hsm + stream_smem_bytes())));
     mid_hist_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm, st>>>(p, tile_rows, tseg, tbase, b_H.as<unsigned int>());
     mid_chunksum_kernel<<<dim3((unsigned int)nchunks, ry), blk, 0, st>>>(R, cseg, tbase, cbase, b_H.as<unsigned int>(),
                                                                          b_P.as<unsigned int>());
@@ -853,8 +962,7 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
   }
   // ---- class M: group counts
   if (nm > 0) {
-    TK_CUDA(cudaFuncSetAttribute(mid_med_count_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-    mid_med_count_kernel<NS><<<(unsigned int)nm, kMidThreads, hsm, st>>>(p, mlist);
+    mid_cta_count_kernel<NS><<<(unsigned int)nm, kMidThreads, (size_t)((R + 31) / 32) * 4, st>>>(p, mlist);
     count_launch();
   }
   // ---- class A: group counts
@@ -870,7 +978,7 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
   if (int rc = scan_excl_i64(p.groups, p.groups, n0, st)) return rc;  // -> out_base, [n0] = groups
   p.out_base = p.groups;
   // ---- every class: straight to the output rows
-  if (nb > 0 || nm > 0)
+  if (nb > 0)
     if (int rc = b_w.alloc((size_t)nnz * 8, st)) return rc;
   if (nb > 0) {
     FoldQueues fq{};
@@ -884,7 +992,7 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
     TK_CUDA(cudaMemsetAsync(b_bign.get(), 0, 64, st));
     fq.q = b_bigq.as<unsigned long long>();
     fq.cnt = b_bign.as<unsigned int>();
-    mid_scatter_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm, st>>>(
+    mid_scatter_kernel<NS><<<(unsigned int)ntiles, kMidThreads, hsm + stream_smem_bytes(), st>>>(
         p, tile_rows, tseg, tbase, isb, b_H.as<unsigned int>(), b_BB.as<unsigned int>(), b_w.as<double>());
     mid_fold_kernel<<<dim3((unsigned int)nb, ry), blk, 0, st>>>(p, blist, b_TOT.as<unsigned int>(), b_BB.as<unsigned int>(),
                                                                 b_GR.as<unsigned int>(), b_w.as<double>(), fq);
@@ -893,8 +1001,9 @@ int mid_run(MidParams& p, bool keep_zeros, int64_t* out_nnz, cudaStream_t st) {
     count_launch(3);
   }
   if (nm > 0) {
-    TK_CUDA(cudaFuncSetAttribute(mid_med_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * hsm)));
-    mid_med_kernel<NS><<<(unsigned int)nm, kMidThreads, 2 * hsm, st>>>(p, mlist, b_w.as<double>());
+    TK_CUDA(cudaFuncSetAttribute(mid_cta_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cta_smem_bytes(R)));
+    mid_cta_kernel<NS><<<(unsigned int)nm, kMidThreads, cta_smem_bytes(R), st>>>(p, mlist);
     count_launch();
   }
   if (na > 0) {
