@@ -7,30 +7,31 @@
 // ORDER (pyx:262-295); exact-zero sums dropped; groups emitted in lexicographic order.
 //
 // The input's leading column is sorted (canonical COO), so segment i0 (the rows with that
-// leading value) is already in place relative to the other segments: only a stable reorder by
-// the suffix key S = (i2, ..., i_{d-1}) (R = prod of those dims <= 2^14) WITHIN each segment is
-// needed.  That is a counting problem over small known dims -- no general sort.  Segments come in
-// three size classes:
-//   * class B (segments > kMedMax rows, the Zipf head): counting tiles of kTileRows rows.  Pass 1
+// leading value) is already in place relative to the other segments: only the rows of equal
+// suffix key S = (i2, ..., i_{d-1}) (R = prod of those dims <= 2^14) WITHIN each segment have to
+// meet, in row order.  That is a counting problem over small known dims -- no general sort.
+// Segments come in three size classes:
+//   * class A (<= kWarpMax rows, the tail: 1e6 segments at config 5): one warp per segment.  A
+//     bitmap of the S present gives every row its group (the rank of its S = its output order);
+//     w = vals * x[i1] is added into acc[group] in row order, 32 rows per step (the first lane of
+//     a group adds the group's rows of the step in lane order).  No sort, no scratch.
+//   * class M (kWarpMax < rows <= kMedMax): one CTA per segment, acc[S] for every possible S in
+//     shared memory.  Chunks of 1024 rows are split stably by OWNER warp (S % 8) into contiguous
+//     shared-memory lists; each warp walks its own list in dense 32-row steps, packs a step by S
+//     and adds every run onto acc[S] left to right.  All rows of one S pass through one warp in
+//     row order, so warps never wait on each other.
+//   * class B (> kMedMax rows, the Zipf head): counting tiles of kTileRows rows.  Pass 1
 //     histograms S per tile in shared memory; a two-level column scan over each segment's tiles
 //     and a scan over S give every (tile, S) its exact row range; pass 2 recomputes w and scatters
-//     it stably -- the eight warps of a tile take 32-row steps in row order, ranks inside a step
-//     come from __match_any_sync, and the warps update the per-S cursors in turn (a token passed
-//     round a ring of named barriers), so every (i0, S) bucket holds its w in original row order;
-//     pass 3 folds every bucket serially (big buckets: coalesced warp loads several chunks ahead,
-//     one lane adds).
-//   * class M (kWin < rows <= kMedMax): one CTA per segment does the same in one tile, with the
-//     bucket cursors and starts in shared memory (no tables): a counting kernel before the output
-//     rows are known, the histogram + stable scatter + bucket folds after.
-//   * class A (segments <= kWin rows, the tail): one CTA per window of kWin class-A rows takes the
-//     class-A segments starting in it (<= 2 kWin rows), sorts their (segment, S) keys in shared
-//     memory with three stable LSD passes (the same token-ring scatter) and folds each group
-//     straight from the staged w; the groups go to a scratch indexed by class-A row and are moved
-//     to their final rows once the per-segment group counts are scanned.
-// Output rows: the groups of every segment (non-empty buckets / distinct S) are exclusive-scanned
-// over i0, so each group knows its output row without any cross-CTA wait.  Every fold is
-// acc = w[first]; acc = __dadd_rn(acc, w[next]) ... in original row order: values bit-identical to
-// the reference.  No library code is used.
+//     it stably with the class-M owner lists (the cursor of S is touched by one warp only, in row
+//     order), so every (i0, S) bucket holds its w in original row order; pass 3 folds every bucket
+//     serially (size bins: one bucket per lane for 64..4095 rows, a whole warp with coalesced
+//     loads far ahead of lane 0's chain for longer ones, longest first by ticket).
+// Output rows: the groups of every segment (distinct S; counted by bitmap kernels for A and M, by
+// the class-B histogram) are exclusive-scanned over i0, so each group knows its output row without
+// any cross-CTA wait.  Every sum is the reference's left fold in original row order with
+// __dadd_rn, started from the first w or from -0.0 (the exact additive identity): values
+// bit-identical to the reference.  No library code is used.
 #include <algorithm>
 #include <vector>
 
@@ -45,7 +46,7 @@ __global__ void lead_offsets_kernel(long long n, const long long* __restrict__ c
 
 namespace {
 
-constexpr int kMidThreads = 256;       // every kernel with a token ring: 8 warps
+constexpr int kMidThreads = 256;       // class B / class M CTAs: 8 warps, warp w owns the S with S % 8 == w
 constexpr int kMidWarps = kMidThreads / 32;
 #ifndef TK_MID_WARPMAX
 #define TK_MID_WARPMAX 512
@@ -54,23 +55,7 @@ constexpr int kWarpMax = TK_MID_WARPMAX;  // class A: segments of at most kWarpM
 constexpr long long kMidMaxR = 16384;  // suffix key S < 2^14
 constexpr int kChunkTiles = 32;        // column scan: tiles per chunk
 constexpr long long kMedMax = 65536;   // class M: segments of kWarpMax+1 .. kMedMax rows
-constexpr long long kTileRows = 262144;  // class B counting tile (long runs per bucket: full-sector writes)
-
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-// warp `warp`'s turn at step `step` of a ring of kMidWarps warps (ids 1..kMidWarps); the first turn
-// is free, and the last warp does not hand over after the last step
-__device__ __forceinline__ void ring_take(int warp, long long step) {
-  if (step > 0 || warp > 0) named_bar_sync(1 + warp, 64);
-}
-__device__ __forceinline__ void ring_pass(int warp, long long step, long long nstep) {
-  if (!(step == nstep - 1 && warp == kMidWarps - 1)) named_bar_arrive(1 + (warp + 1) % kMidWarps, 64);
-}
+constexpr long long kTileRows = 262144;  // class B counting tile (32K..256K rows measure the same; fewer tiles = smaller tables)
 
 struct MidParams {
   long long nnz, n0, n1, R;

@@ -952,12 +952,17 @@ def test_nccl_comm_inside_the_library_single_rank():
     ((30, 40, 20, 10), 150_000, 1.2, {}),                            # order 4, class M
     ((3000, 20, 30), 400_000, 0.0, {}),                              # class A only
     ((200000, 50, 40), 300_000, 0.0, {}),                            # tiny segments, empty leading values
+    ((40, 3000, 2), 200_000, 1.1, {}),                               # R = 2: one or two owner warps, long single-S chains
+    ((6, 200000, 1), 900_000, 0.0, {"TK_MID_MEDMAX": "4096"}),       # R = 1: every row one S (classes M and B, 150K-row chains)
+    ((30, 50, 16384), 300_000, 0.0, {}),                             # R = 2^14: the widest accumulator array
+    ((700, 40, 600), 700_000, 0.9, {}),                              # segments around the class A / M boundary (512 rows)
 ])
 def test_middle_mode_counting_path_bit_exact(oracle, monkeypatch, shape, nnz, zipf, env):
     """k == 1 (the paper's middle-mode protocol) through the segmented counting path
-    (tk_midmode.cu): class-A warp sorts, class-B counting tiles with the warp token ring and the
-    bucket folds -- bit-exact against the oracle, with the class thresholds shrunk to put most
-    rows through class B."""
+    (tk_midmode.cu): class-A warp-per-segment accumulation, class-M owner lists with in-place
+    accumulators, class-B counting tiles, owner-list scatter and the binned bucket folds --
+    bit-exact against the oracle, with the class thresholds shrunk to put small data through every
+    class and many tiles."""
     import paper_2510_01495_b200 as tk
     for kk, vv in env.items():
         monkeypatch.setenv(kk, vv)
