@@ -457,16 +457,22 @@ def secondary_measurements(rank, steps, threads, with_cpu):
             if i >= 2:
                 ts.append(e0.elapsed_time(e1))
         return float(np.median(ts)), u, (lib.tk_launch_count() - l0) / 5
-    ms, u5, launches = time_k1()  # the segmented counting path (tk_midmode.cu), no library sort
+    ms, u5, launches = time_k1()  # the segmented path (tk_midmode.cu), no library sort
     b = c5["nnz"] * 32 + 8 * c5["shape"][1] + u5 * 24
     res["cfg5_ttv_mode1_sort_path"] = {"call_ms": ms, "GBps": b / ms / 1e6, "nnz_per_s": c5["nnz"] / ms * 1e3,
                                        "bytes": b, "u": u5, "launches_per_call": launches,
-                                       "path": "segmented counting by the suffix key (tk_midmode.cu)"}
+                                       "path": "per leading value: in-order accumulation by the suffix key (warp / CTA "
+                                               "accumulators; the largest segments by a stable owner-list scatter + "
+                                               "serial bucket folds), tk_midmode.cu"}
+    keep = (o_s5[:u5].clone(), o_v5[:u5].clone())
     os.environ["TK_MID_MODE"] = "0"  # the previous path, for comparison: CUB stable radix sort per interval
     try:
-        ms0, _, launches0 = time_k1()
+        ms0, u0, launches0 = time_k1()
     finally:
         os.environ.pop("TK_MID_MODE", None)
+    same = bool(u0 == u5 and torch.equal(keep[0], o_s5[:u0]) and torch.equal(keep[1].view(torch.int64), o_v5[:u0].view(torch.int64)))
+    res["cfg5_ttv_mode1_sort_path"]["bit_identical_to_cub_split_path"] = same
+    del keep
     res["cfg5_ttv_mode1_cub_split_path"] = {"call_ms": ms0, "GBps": b / ms0 / 1e6, "launches_per_call": launches0,
                                             "path": "interval split + cub::DeviceRadixSort (TK_MID_MODE=0)"}
     del t5, o_s5, o_v5

@@ -14,3 +14,6 @@ echo "launch list rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:ttv_tile -s 1 -c 1 -f \
   -o gpurun_out/${tag}_tile python tools/prof_ttv.py --what cfg5 --nnz 400000000 --iters 2 > gpurun_out/${tag}_ncu_full.log 2>&1
 echo "full capture rc=$?"
+# the middle-mode path (config 5, k = 1): per-kernel times of one call (ncu launch list, six calls averaged)
+bash tools/launches_mid.sh > gpurun_out/${tag}_launches_mid.txt 2>&1
+echo "mid launch list rc=$?"
