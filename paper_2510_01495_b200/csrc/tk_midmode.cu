@@ -88,6 +88,28 @@ __device__ __forceinline__ long long suffix_key(const MidParams& p, long long r,
   return s;
 }
 
+// The suffix key for pipelined loads: nothing here waits on the loaded value when there is one
+// suffix column (the usual 3-way tensor) -- the consumer checks it against R later with
+// suffix_check.  With several suffix columns the key is combined at once; -1 = out of range.
+template <int NS>
+__device__ __forceinline__ long long suffix_load(const MidParams& p, long long r) {
+  if (NS == 1) return __ldcs(p.sc[0] + r);
+  const int ns = NS > 0 ? NS : p.ns;
+  long long s = 0;
+  bool oob = false;
+  for (int j = 0; j < ns; ++j) {
+    const long long v = __ldcs(p.sc[j] + r);
+    oob = oob || (unsigned long long)v >= (unsigned long long)p.sdim[j];
+    s = s * p.sdim[j] + v;
+  }
+  return oob ? -1 : s;
+}
+// a loaded suffix key -> [0, R); out of range: flagged (the call declines), clamped for memory safety
+__device__ __forceinline__ long long suffix_check(const MidParams& p, long long s, bool live, unsigned int& flags) {
+  if (live && (unsigned long long)s >= (unsigned long long)p.R) flags |= kFlagKeptOob;
+  return max(0LL, min(s, p.R - 1));
+}
+
 __device__ __forceinline__ double row_w(const MidParams& p, long long r, unsigned int& flags) {
   const long long i1 = __ldg(p.c1 + r);
   const bool bad = (unsigned long long)i1 >= (unsigned long long)p.n1;
@@ -282,7 +304,7 @@ __device__ __forceinline__ void stream_owned(const MidParams& p, long long r0, l
     for (int k = 0; k < kRowsPerThread; ++k) {
       const long long r = cbase + k * kMidThreads + tid;
       if (r < r1) {
-        sA[k] = suffix_key<NS>(p, r, flags);
+        sA[k] = suffix_load<NS>(p, r);
         iA[k] = __ldcs(p.c1 + r);
         vA[k] = __ldcs(p.vals + r);
       } else {
@@ -298,7 +320,7 @@ __device__ __forceinline__ void stream_owned(const MidParams& p, long long r0, l
       const long long r = cbase + k * kMidThreads + tid;
       const bool bad = (unsigned long long)iA[k] >= (unsigned long long)p.n1;
       if (bad && r < r1) flags |= kFlagIndex;
-      sB[k] = (unsigned short)max(0LL, min(sA[k], p.R - 1));  // out of range: flagged by suffix_key, the call declines
+      sB[k] = (unsigned short)suffix_check(p, sA[k], r < r1, flags);
       vB[k] = vA[k];
       xB[k] = __ldg(p.x + (bad || r >= r1 ? 0 : iA[k]));
     }
@@ -820,7 +842,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p
     long long sn = 0, i1n = 0;
     double vn = 0.0;
     if (lane < L) {
-      sn = suffix_key<NS>(p, r0 + lane, flags);
+      sn = suffix_load<NS>(p, r0 + lane);
       i1n = __ldcs(p.c1 + r0 + lane);
       vn = __ldcs(p.vals + r0 + lane);
     }
@@ -830,7 +852,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p
       const long long s = max(0LL, min(sn, p.R - 1)), i1 = i1n;
       const double v = vn;
       if (j + 32 < L) {
-        sn = suffix_key<NS>(p, r0 + j + 32, flags);
+        sn = suffix_load<NS>(p, r0 + j + 32);
         i1n = __ldcs(p.c1 + r0 + j + 32);
         vn = __ldcs(p.vals + r0 + j + 32);
       }
