@@ -973,6 +973,27 @@ def test_middle_mode_counting_path_bit_exact(oracle, monkeypatch, shape, nnz, zi
     assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes() and len(ev) > 0
 
 
+def test_middle_mode_exact_class_boundaries(oracle):
+    """Segments of exactly 1, 2, 31, 32, 33, 511, 512, 513, 1023, 1024, 1025, 65535, 65536 and
+    65537 rows (the class A / M / B thresholds and the 32-row step and 1024-row chunk edges), with
+    empty leading values in between -- bit-exact against the oracle."""
+    import paper_2510_01495_b200 as tk
+    rng = np.random.default_rng(23)
+    n1, n2 = 300, 300
+    sizes = [1, 0, 2, 31, 32, 33, 0, 0, 511, 512, 513, 1023, 1024, 1025, 65535, 65536, 65537, 0, 7]
+    rows = []
+    for i0, L in enumerate(sizes):
+        flat = np.sort(rng.choice(n1 * n2, size=L, replace=False))
+        rows.append(np.stack([np.full(L, i0), flat // n2, flat % n2], axis=1))
+    s = np.concatenate(rows).astype(np.int64)
+    v = rng.standard_normal(len(s))
+    shape = (len(sizes), n1, n2)
+    x = oracle.gen_uniform(n1, 9)
+    es, ev, _ = oracle.ttv_raw(s, v, shape, x, 1)
+    gs, gv, _ = tk.kernels().ttv_raw(s, v, shape, x, 1)
+    assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes() and len(ev) > 0
+
+
 def test_middle_mode_zero_groups_errors_and_declines(oracle):
     """Exact-zero groups are removed (compaction), an out-of-range contracted index raises
     DimensionError, garbage kept indices and an unsorted leading column decline to the general
