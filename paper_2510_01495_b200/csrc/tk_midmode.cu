@@ -805,10 +805,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p
   unsigned short* skey = pre + W;
   const int K = (W + 31) >> 5;  // bitmap words per lane in the rank scan
   unsigned int flags = 0, zeros = 0;
-  for (long long q = (long long)blockIdx.x * kWarpsPerCta + warp; q < nseg; q += (long long)gridDim.x * kWarpsPerCta) {
-    const int i0 = alist[q];
-    const long long r0 = p.off[i0];
-    const int L = (int)(p.off[i0 + 1] - r0);
+  // A segment costs a few dependent DRAM round trips (list entry -> offsets -> rows), so the warp
+  // works one segment ahead: while segment q is processed, the rows of its next segment are being
+  // prefetched into L2 (lane l takes the l-th 128-byte line of each column: 512 rows) and the list
+  // entry and offsets of the one after are in flight.
+  const long long qstride = (long long)gridDim.x * kWarpsPerCta;
+  const long long q0 = (long long)blockIdx.x * kWarpsPerCta + warp;
+  auto seg_of = [&](long long q, int& i0, long long& r0, int& L) {
+    i0 = q < nseg ? alist[q] : -1;
+    r0 = i0 >= 0 ? p.off[i0] : 0;
+    L = i0 >= 0 ? (int)(p.off[i0 + 1] - r0) : 0;
+  };
+  auto prefetch_rows = [&](long long r0, int L) {
+    if (L <= 0) return;
+    const int ns = COUNT ? 0 : 2;  // COUNT reads only the suffix columns
+    for (int c = 0; c < ns + (NS > 0 ? NS : p.ns); ++c) {
+      const char* col = c < ns ? (c == 0 ? (const char*)p.c1 : (const char*)p.vals) : (const char*)p.sc[c - ns];
+      const char* a = col + r0 * 8, *e = a + (long long)L * 8;
+      const char* line = (const char*)((unsigned long long)a & ~127ull) + 128 * lane;
+      if (line < e) asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
+    }
+  };
+  int i0n, Ln, i0nn, Lnn;
+  long long r0n, r0nn;
+  seg_of(q0, i0n, r0n, Ln);
+  seg_of(q0 + qstride, i0nn, r0nn, Lnn);
+  for (long long q = q0; q < nseg; q += qstride) {
+    const int i0 = i0n;
+    const long long r0 = r0n;
+    const int L = Ln;
+    i0n = i0nn, r0n = r0nn, Ln = Lnn;
+    prefetch_rows(r0n, Ln);
+    seg_of(q + 2 * qstride, i0nn, r0nn, Lnn);
     for (int i = lane; i < W; i += 32) bm[i] = 0;
     __syncwarp();
     for (int j = lane; j < L; j += 32) {
