@@ -837,6 +837,29 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p
     i0n = i0nn, r0n = r0nn, Ln = Lnn;
     prefetch_rows(r0n, Ln);
     seg_of(q + 2 * qstride, i0nn, r0nn, Lnn);
+    if constexpr (COUNT) {
+      // the count alone needs no rank scan: exactly one row per distinct S finds its bit clear when
+      // it sets it; the bits are cleared again row by row (the bitmap starts and stays zero)
+      if (q == q0)
+        for (int i = lane; i < W; i += 32) bm[i] = 0;
+      __syncwarp();
+      int firsts = 0;
+      for (int j = lane; j < L; j += 32) {
+        const long long s = max(0LL, min(suffix_key<NS>(p, r0 + j, flags), p.R - 1));
+        const unsigned int bit = 1u << (s & 31);
+        firsts += !(atomicOr(&bm[s >> 5], bit) & bit);
+      }
+      firsts = __reduce_add_sync(0xffffffffu, firsts);
+      if (lane == 0) p.groups[i0] = firsts;
+      __syncwarp();
+      for (int j = lane; j < L; j += 32) {  // the rows again (L1-resident): clear what they set
+        unsigned int dummy = 0;
+        const long long s = max(0LL, min(suffix_key<NS>(p, r0 + j, dummy), p.R - 1));
+        bm[s >> 5] = 0;
+      }
+      __syncwarp();
+      continue;
+    }
     for (int i = lane; i < W; i += 32) bm[i] = 0;
     __syncwarp();
     for (int j = lane; j < L; j += 32) {
@@ -856,11 +879,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mid_warp_kernel(MidParams p
       if (lane >= o) incl += v;
     }
     const int G = __shfl_sync(0xffffffffu, incl, 31);
-    if constexpr (COUNT) {
-      if (lane == 0) p.groups[i0] = G;
-      __syncwarp();
-      continue;
-    }
     int run = incl - cnt;
     for (int k = 0; k < K; ++k) {
       const int i = lane * K + k;
