@@ -907,6 +907,36 @@ def test_tile_three_pass_fallback_bit_exact(oracle, monkeypatch, golden_small, g
         assert s.tobytes() == es.tobytes() and v.tobytes() == ev.tobytes(), k
 
 
+def test_tile_kernel_beside_concurrent_kernels(oracle):
+    """The single-pass tile kernel relies on its blocks being dispatched in index order while it
+    shares the GPU: with another stream keeping every SM busy (back-to-back GEMMs and copies) the
+    device-resident TTV -- sorted-stream path and the middle-mode path -- is still bit-exact
+    against the oracle, call after call (a stalled wait would re-run the call as three passes or
+    fail it; either way the result must be right)."""
+    import torch
+    from paper_2510_01495_b200.device import DeviceCoo
+    shape = (3000, 500, 600)
+    subs, vals = oracle.gen_coo(shape, 6_000_000, zipf_s=1.2, normal_vals=True, seed=31)
+    t = DeviceCoo.from_host(subs, vals, shape)
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    big = torch.empty(64 * 2**20, device="cuda", dtype=torch.float32)
+    for k in (2, 1):
+        x_h = oracle.gen_uniform(shape[k], 40 + k)
+        es, ev, _ = oracle.ttv_raw(subs, vals, shape, x_h, k)
+        x = torch.from_numpy(x_h).cuda()
+        torch.cuda.synchronize()
+        for rep in range(4):
+            with torch.cuda.stream(side):  # ~20 ms of work on the other stream, queued first
+                for _ in range(12):
+                    b = a @ a
+                    big.add_(1.0)
+            u, os_d, ov_d = t.ttv(x, k)
+            gs, gv = os_d[:u].cpu().numpy(), ov_d[:u].cpu().numpy()
+            assert gs.tobytes() == es.tobytes() and gv.tobytes() == ev.tobytes(), (k, rep)
+        torch.cuda.synchronize()
+
+
 def test_nccl_comm_inside_the_library_single_rank():
     """The C-ABI NCCL data plane (tk_nccl_*) on the one GPU of the test box: a one-rank
     communicator runs every exchange the sharded TTV uses -- the count all-gather (pipelined
